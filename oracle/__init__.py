@@ -1,0 +1,266 @@
+"""ctypes wrapper of the CPU oracle (oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, never by the product package
+(paper_2203_11484_b200).  See oracle.c's header for the arithmetic contract.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+SRC = HERE / "oracle.c"
+LIB = HERE / "liboracle.so"
+
+CFLAGS = ["-O3", "-march=x86-64-v3", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+          "-fPIC", "-shared", "-std=c11", "-Wall", "-Wno-unused-function"]
+
+VPL_DTYPE = np.dtype([("pos", "<f4", 3), ("nrm", "<f4", 3), ("flux", "<f4", 3),
+                      ("tri", "<i4"), ("tag", "<i4"), ("depth", "<i4"), ("walk", "<i4")])
+GBUF_DTYPE = np.dtype([("pos", "<f4", 3), ("nrm", "<f4", 3), ("alb", "<f4", 3), ("t", "<f4"),
+                       ("tri", "<i4"), ("front", "<i4")])
+
+FLAG_EMPTY_NEAR, FLAG_EMPTY_FAR, FLAG_WALK_BUDGET_UNMET = 1, 2, 4
+
+
+class OParams(C.Structure):
+    _fields_ = [("M", C.c_int64), ("K_near", C.c_int64), ("max_depth", C.c_int64), ("rr", C.c_int64),
+                ("n_walks_fixed", C.c_int64), ("seed", C.c_uint64)]
+
+
+class OInfo(C.Structure):
+    _fields_ = [("n_near", C.c_int64), ("n_lit", C.c_int64), ("K", C.c_int64), ("M_far", C.c_int64),
+                ("n_walks", C.c_int64), ("flags", C.c_int64), ("n_far_tris", C.c_int64),
+                ("n_out", C.c_int64)]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
+def build(force: bool = False) -> Path:
+    if force or not LIB.exists() or LIB.stat().st_mtime < SRC.stat().st_mtime:
+        tmp = LIB.with_suffix(f".{os.getpid()}.tmp.so")
+        subprocess.check_call(["gcc", *CFLAGS, "-o", str(tmp), str(SRC), "-lm"])
+        os.replace(tmp, LIB)
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(str(LIB))
+        P, I64, F, U8, U32, U64 = C.c_void_p, C.c_int64, C.c_float, C.c_uint8, C.c_uint32, C.c_uint64
+        sig = {
+            "oracle_philox4x32_10": (None, [P, P, P]),
+            "oracle_draw": (U32, [U64, U32, U32, U32]),
+            "oracle_scene_new": (P, [P, P, I64, P, C.c_int, P, C.c_int, C.c_int]),
+            "oracle_scene_free": (None, [P]),
+            "oracle_scene_bad": (I64, [P]),
+            "oracle_scene_consts": (None, [P, P, P, P]),
+            "oracle_tri_data": (None, [P, P, P, P, P]),
+            "oracle_closest_hit": (I64, [P, P, P, F, F, P]),
+            "oracle_occluded": (C.c_int, [P, P, P]),
+            "oracle_occluded_batch": (None, [P, P, P, I64, P]),
+            "oracle_closest_batch": (None, [P, P, P, I64, F, F, P, P]),
+            "oracle_classify": (None, [P, C.c_double, P, P]),
+            "oracle_lit": (None, [P, P, P]),
+            "oracle_morton3": (U32, [U32, U32, U32]),
+            "oracle_near_table": (I64, [P, P, P, P, P]),
+            "oracle_stratum": (U64, [U64, I64, I64, U64]),
+            "oracle_lookup_g": (I64, [P, I64, U64]),
+            "oracle_point_in_tri": (None, [P, I64, F, F, P]),
+            "oracle_generate_vpls": (I64, [P, P, P, P, I64, P]),
+            "oracle_gbuffer": (None, [P, P, I64, P]),
+            "oracle_gather": (None, [P, P, I64, P, I64, P, P, P, P, P]),
+            "oracle_pair_visibility": (None, [P, P, P, I64, P]),
+            "oracle_abi": (C.c_int, []),
+            "oracle_threads": (C.c_int, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def philox(ctr, key):
+    c = np.asarray(ctr, np.uint32).copy()
+    k = np.asarray(key, np.uint32).copy()
+    out = np.zeros(4, np.uint32)
+    lib().oracle_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def draw(seed, stream, item, j):
+    return int(lib().oracle_draw(seed, stream, item, j))
+
+
+def morton3(qx, qy, qz):
+    return int(lib().oracle_morton3(qx, qy, qz))
+
+
+def stratum(seed, k, K, F):
+    return int(lib().oracle_stratum(seed, k, K, F))
+
+
+def lookup_g(P: np.ndarray, s: int) -> int:
+    P = np.ascontiguousarray(P, np.uint64)
+    return int(lib().oracle_lookup_g(_p(P), P.size, s))
+
+
+def threads() -> int:
+    return int(lib().oracle_threads())
+
+
+class OracleScene:
+    """Oracle view of a scenegen.Scene (or raw arrays)."""
+
+    def __init__(self, scene):
+        self.scene = scene
+        self._keep = [np.ascontiguousarray(scene.verts, np.float32),
+                      np.ascontiguousarray(scene.albedo, np.float32),
+                      np.ascontiguousarray(scene.lights, np.float32).reshape(-1, 16),
+                      np.ascontiguousarray(scene.cam, np.float32)]
+        V, A, Lt, Cm = self._keep
+        self.n = V.shape[0]
+        self.h = lib().oracle_scene_new(_p(V), _p(A), self.n, _p(Lt), Lt.shape[0], _p(Cm),
+                                        scene.width, scene.height)
+        if not self.h:
+            raise ValueError("oracle_scene_new failed")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().oracle_scene_free(self.h)
+            self.h = None
+
+    # ---- O1 ----
+    @property
+    def bad(self) -> int:
+        return int(lib().oracle_scene_bad(self.h))
+
+    def consts(self):
+        d, e, b = C.c_double(), C.c_float(), C.c_float()
+        lib().oracle_scene_consts(self.h, C.byref(d), C.byref(e), C.byref(b))
+        return d.value, np.float32(e.value), np.float32(b.value)
+
+    def tri_data(self):
+        n = self.n
+        nrm, cen = np.zeros((n, 3), np.float32), np.zeros((n, 3), np.float32)
+        area, aq = np.zeros(n, np.float32), np.zeros(n, np.uint64)
+        lib().oracle_tri_data(self.h, _p(nrm), _p(cen), _p(area), _p(aq))
+        return dict(normal=nrm, centroid=cen, area=area, aq=aq)
+
+    # ---- O9 ----
+    def closest_hit(self, o, d, tmin=0.0, tmax=np.inf):
+        o = np.asarray(o, np.float32); d = np.asarray(d, np.float32)
+        t = C.c_float()
+        i = lib().oracle_closest_hit(self.h, _p(o), _p(d), tmin, tmax, C.byref(t))
+        return int(i), np.float32(t.value)
+
+    def closest_batch(self, o, d, tmin=0.0, tmax=np.inf):
+        o = np.ascontiguousarray(o, np.float32).reshape(-1, 3)
+        d = np.ascontiguousarray(d, np.float32).reshape(-1, 3)
+        idx, t = np.zeros(len(o), np.int64), np.zeros(len(o), np.float32)
+        lib().oracle_closest_batch(self.h, _p(o), _p(d), len(o), tmin, tmax, _p(idx), _p(t))
+        return idx, t
+
+    def occluded(self, a, b) -> bool:
+        a = np.asarray(a, np.float32); b = np.asarray(b, np.float32)
+        return bool(lib().oracle_occluded(self.h, _p(a), _p(b)))
+
+    def occluded_batch(self, a, b):
+        a = np.ascontiguousarray(a, np.float32).reshape(-1, 3)
+        b = np.ascontiguousarray(b, np.float32).reshape(-1, 3)
+        out = np.zeros(len(a), np.uint8)
+        lib().oracle_occluded_batch(self.h, _p(a), _p(b), len(a), _p(out))
+        return out.astype(bool)
+
+    # ---- O2 ----
+    def classify(self, T=None):
+        T = self.scene.T if T is None else T
+        labels = np.zeros(self.n, np.uint8)
+        nn = C.c_int64()
+        lib().oracle_classify(self.h, float(T), _p(labels), C.byref(nn))
+        return labels, int(nn.value)
+
+    # ---- O3-O5 ----
+    def lit(self, labels):
+        labels = np.ascontiguousarray(labels, np.uint8)
+        out = np.zeros(self.n, np.uint8)
+        lib().oracle_lit(self.h, _p(labels), _p(out))
+        return out
+
+    def near_table(self, lit):
+        lit = np.ascontiguousarray(lit, np.uint8)
+        order, P = np.zeros(self.n, np.int64), np.zeros(self.n, np.uint64)
+        codes = np.zeros(self.n, np.uint32)
+        m = lib().oracle_near_table(self.h, _p(lit), _p(order), _p(P), _p(codes))
+        return order[:m], P[:m], codes[:m]
+
+    def point_in_tri(self, t, u1, u2):
+        out = np.zeros(3, np.float32)
+        lib().oracle_point_in_tri(self.h, int(t), float(u1), float(u2), _p(out))
+        return out
+
+    # ---- O3-O11 ----
+    def generate_vpls(self, labels, M=None, K_near=None, max_depth=None, rr=None, seed=None,
+                      n_walks_fixed=0, max_out=None):
+        s = self.scene
+        p = OParams(M=s.M if M is None else M, K_near=s.K_near if K_near is None else K_near,
+                    max_depth=s.max_depth if max_depth is None else max_depth,
+                    rr=s.rr if rr is None else rr, n_walks_fixed=n_walks_fixed,
+                    seed=s.seed if seed is None else seed)
+        cap = max_out if max_out is not None else max(p.M, 1) + (n_walks_fixed * max(p.max_depth, 1))
+        out = np.zeros(cap, VPL_DTYPE)
+        info = OInfo()
+        labels = np.ascontiguousarray(labels, np.uint8)
+        n = lib().oracle_generate_vpls(self.h, _p(labels), C.byref(p), _p(out), cap, C.byref(info))
+        if n < 0:
+            raise RuntimeError("oracle_generate_vpls: output capacity too small")
+        return out[:n].copy(), info.as_dict()
+
+    # ---- O12 ----
+    def gbuffer(self, pixels):
+        pixels = np.ascontiguousarray(pixels, np.int32)
+        out = np.zeros(len(pixels), GBUF_DTYPE)
+        lib().oracle_gbuffer(self.h, _p(pixels), len(pixels), _p(out))
+        return out
+
+    # ---- O13 ----
+    def gather(self, gb, vpls, bits=False):
+        gb = np.ascontiguousarray(gb, GBUF_DTYPE)
+        vpls = np.ascontiguousarray(vpls, VPL_DTYPE)
+        n, M = len(gb), len(vpls)
+        rgb = np.zeros((n, 3), np.float32)
+        rgb64 = np.zeros((n, 3), np.float64)
+        traced = C.c_int64()
+        words = (M + 31) // 32
+        tb = np.zeros((n, words), np.uint32) if bits else None
+        vb = np.zeros((n, words), np.uint32) if bits else None
+        lib().oracle_gather(self.h, _p(gb), n, _p(vpls), M, _p(rgb), _p(rgb64), C.byref(traced),
+                            _p(tb) if bits else None, _p(vb) if bits else None)
+        res = dict(rgb=rgb, rgb64=rgb64, traced=int(traced.value))
+        if bits:
+            res["traced_bits"], res["vis_bits"] = tb, vb
+        return res
+
+    def pair_visibility(self, x, y):
+        x = np.ascontiguousarray(x, np.float32).reshape(-1, 3)
+        y = np.ascontiguousarray(y, np.float32).reshape(-1, 3)
+        out = np.zeros(len(x), np.uint8)
+        lib().oracle_pair_visibility(self.h, _p(x), _p(y), len(x), _p(out))
+        return out.astype(bool)

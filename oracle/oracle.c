@@ -1,0 +1,742 @@
+/*
+ * oracle.c — plain, slow, obviously-correct CPU oracle for the hybrid-VPL
+ * many-light gather of arXiv 2203.11484 (PAPER.md = P, line numbers P:n).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  It
+ * shares no code with the CUDA path (paper_2203_11484_b200/csrc) and includes
+ * none of its headers; both sides implement DESIGN.md §3 independently.
+ *
+ * Arithmetic contract (DESIGN.md §3 O0): IEEE binary32, round-to-nearest,
+ * compiled with -ffp-contract=off (no FMA contraction), no fast-math, only
+ * + - * / sqrt on floats.  Every loop follows the paper's definition; the
+ * only library primitives are qsort (the Morton sort of P:62-63) and libm
+ * nearbyint/sqrt in double for host constants.  Visibility and closest hit
+ * are brute force over all triangles (no BVH).  Loops over independent
+ * rays/pixels/walks are OpenMP-parallel; no per-pixel sum is reordered.
+ *
+ * Parity pins: see tests/test_oracle_*.py (closed forms, invariants, Philox
+ * vs the CUDA toolkit's host Philox, brute-force tiny scenes).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_ABI 1
+#define PI_D 3.14159265358979323846 /* pi, rounded once to double */
+
+typedef struct { float x, y, z; } f3;
+
+static inline f3 mk(float x, float y, float z) { f3 r = {x, y, z}; return r; }
+static inline f3 add(f3 a, f3 b) { return mk(a.x + b.x, a.y + b.y, a.z + b.z); }
+static inline f3 sub(f3 a, f3 b) { return mk(a.x - b.x, a.y - b.y, a.z - b.z); }
+static inline f3 scl(float s, f3 a) { return mk(s * a.x, s * a.y, s * a.z); }
+/* dot(a,b) = (a.x*b.x + a.y*b.y) + a.z*b.z  (O0) */
+static inline float dot(f3 a, f3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+static inline f3 cross(f3 a, f3 b) {
+    return mk(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+static inline f3 ld3(const float* p) { return mk(p[0], p[1], p[2]); }
+
+/* ------------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon et al., SC'11): 10 rounds, multipliers 0xD2511F53,  */
+/* 0xCD9E8D57, Weyl key bumps 0x9E3779B9, 0xBB67AE85.                        */
+/* ------------------------------------------------------------------------ */
+void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int r = 0; r < 10; r++) {
+        if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+        uint32_t n1 = (uint32_t)p1;
+        uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+        uint32_t n3 = (uint32_t)p0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Draw j of (stream, item): counter = (j>>2, item, stream, 0), key = seed
+ * split into (lo, hi); lane j & 3 (DESIGN.md §3 O0).                        */
+uint32_t oracle_draw(uint64_t seed, uint32_t stream, uint32_t item, uint32_t j) {
+    uint32_t ctr[4] = {j >> 2, item, stream, 0u};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t out[4];
+    oracle_philox4x32_10(ctr, key, out);
+    return out[j & 3u];
+}
+/* u32 -> float in [0, 1 - 2^-24], exact */
+static inline float u01(uint32_t x) { return (float)(x >> 8) * 0x1p-24f; }
+
+enum { STREAM_NEAR = 0, STREAM_WALK = 1 };
+
+/* ------------------------------------------------------------------------ */
+/* Scene                                                                     */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int64_t n;
+    int nL, W, H;
+    /* SoA copies for brute-force intersection */
+    float *v0x, *v0y, *v0z, *e1x, *e1y, *e1z, *e2x, *e2y, *e2z;
+    float *nrm;   /* [3n] unit normal (O1) */
+    float *cen;   /* [3n] centroid (O1) */
+    float *area;  /* [n] */
+    uint64_t *aq; /* [n] 40-bit fixed-point area */
+    float *alb;   /* [3n] */
+    float *vert;  /* [9n] */
+    float lights[16 * 64];
+    float cam[14];
+    int64_t bad;  /* -1 or first degenerate triangle */
+    double diag;
+    float eps, b2;
+} OScene;
+
+/* O1 — per-triangle prep. */
+static void tri_prep(OScene* s, int64_t i) {
+    const float* v = s->vert + 9 * i;
+    f3 v0 = ld3(v), v1 = ld3(v + 3), v2 = ld3(v + 6);
+    f3 e1 = sub(v1, v0), e2 = sub(v2, v0);
+    s->v0x[i] = v0.x; s->v0y[i] = v0.y; s->v0z[i] = v0.z;
+    s->e1x[i] = e1.x; s->e1y[i] = e1.y; s->e1z[i] = e1.z;
+    s->e2x[i] = e2.x; s->e2y[i] = e2.y; s->e2z[i] = e2.z;
+    f3 c = cross(e1, e2);
+    float len = sqrtf(dot(c, c));
+    float area = 0.5f * len;
+    s->area[i] = area;
+    s->nrm[3 * i + 0] = c.x / len;
+    s->nrm[3 * i + 1] = c.y / len;
+    s->nrm[3 * i + 2] = c.z / len;
+    f3 ce = add(add(v0, v1), v2);
+    s->cen[3 * i + 0] = ce.x / 3.0f;
+    s->cen[3 * i + 1] = ce.y / 3.0f;
+    s->cen[3 * i + 2] = ce.z / 3.0f;
+    double a40 = (double)area * 1099511627776.0; /* exact: power-of-two scale */
+    s->aq[i] = (uint64_t)nearbyint(a40);           /* round half to even     */
+}
+
+void oracle_scene_free(OScene* s) {
+    if (!s) return;
+    float* arrs[] = {s->v0x, s->v0y, s->v0z, s->e1x, s->e1y, s->e1z, s->e2x, s->e2y, s->e2z,
+                     s->nrm, s->cen, s->area, s->alb, s->vert};
+    for (unsigned k = 0; k < sizeof(arrs) / sizeof(arrs[0]); k++) free(arrs[k]);
+    free(s->aq);
+    free(s);
+}
+
+OScene* oracle_scene_new(const float* verts, const float* albedo, int64_t n, const float* lights,
+                         int nL, const float* cam, int W, int H) {
+    if (n <= 0 || nL < 0 || nL > 64) return NULL;
+    OScene* s = (OScene*)calloc(1, sizeof(OScene));
+    s->n = n; s->nL = nL; s->W = W; s->H = H;
+    float** soa[] = {&s->v0x, &s->v0y, &s->v0z, &s->e1x, &s->e1y, &s->e1z, &s->e2x, &s->e2y, &s->e2z,
+                     &s->area};
+    for (unsigned k = 0; k < sizeof(soa) / sizeof(soa[0]); k++) *soa[k] = (float*)malloc(sizeof(float) * n);
+    s->nrm = (float*)malloc(sizeof(float) * 3 * n);
+    s->cen = (float*)malloc(sizeof(float) * 3 * n);
+    s->alb = (float*)malloc(sizeof(float) * 3 * n);
+    s->vert = (float*)malloc(sizeof(float) * 9 * n);
+    s->aq = (uint64_t*)malloc(sizeof(uint64_t) * n);
+    memcpy(s->vert, verts, sizeof(float) * 9 * n);
+    memcpy(s->alb, albedo, sizeof(float) * 3 * n);
+    if (nL) memcpy(s->lights, lights, sizeof(float) * 16 * nL);
+    memcpy(s->cam, cam, sizeof(float) * 14);
+    s->bad = -1;
+    for (int64_t i = 0; i < n; i++) {
+        tri_prep(s, i);
+        if (s->bad < 0 && (!(s->area[i] > 0.0f) || s->aq[i] == 0)) s->bad = i;
+    }
+    /* scene diagonal over all vertices (R12/R13 constants, in double) */
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = 0; i < 3 * n; i++)
+        for (int a = 0; a < 3; a++) {
+            float x = s->vert[3 * i + a];
+            if (x < lo[a]) lo[a] = x;
+            if (x > hi[a]) hi[a] = x;
+        }
+    double dx = (double)hi[0] - (double)lo[0], dy = (double)hi[1] - (double)lo[1],
+           dz = (double)hi[2] - (double)lo[2];
+    s->diag = sqrt(dx * dx + dy * dy + dz * dz);
+    s->eps = (float)(1e-4 * s->diag);                               /* R13 */
+    s->b2 = (float)((0.01 * s->diag) * (0.01 * s->diag));           /* R12 */
+    return s;
+}
+
+int64_t oracle_scene_bad(const OScene* s) { return s->bad; }
+void oracle_scene_consts(const OScene* s, double* diag, float* eps, float* b2) {
+    *diag = s->diag; *eps = s->eps; *b2 = s->b2;
+}
+void oracle_tri_data(const OScene* s, float* nrm, float* cen, float* area, uint64_t* aq) {
+    memcpy(nrm, s->nrm, sizeof(float) * 3 * s->n);
+    memcpy(cen, s->cen, sizeof(float) * 3 * s->n);
+    memcpy(area, s->area, sizeof(float) * s->n);
+    memcpy(aq, s->aq, sizeof(uint64_t) * s->n);
+}
+
+/* ------------------------------------------------------------------------ */
+/* O9 — Moller-Trumbore, brute force over every triangle.                    */
+/* hit(i) <=> det != 0 & u>=0 & u<=1 & v>=0 & u+v<=1 & tmin<t & t<tmax       */
+/* ------------------------------------------------------------------------ */
+#define CHUNK 2048
+
+static int any_hit_chunk(const OScene* s, f3 o, f3 d, float tmin, float tmax, int64_t i0, int64_t i1) {
+    int hit = 0;
+    for (int64_t i = i0; i < i1; i++) {
+        float e1x = s->e1x[i], e1y = s->e1y[i], e1z = s->e1z[i];
+        float e2x = s->e2x[i], e2y = s->e2y[i], e2z = s->e2z[i];
+        float pvx = d.y * e2z - d.z * e2y;
+        float pvy = d.z * e2x - d.x * e2z;
+        float pvz = d.x * e2y - d.y * e2x;
+        float det = (e1x * pvx + e1y * pvy) + e1z * pvz;
+        float inv = 1.0f / det;
+        float sx = o.x - s->v0x[i], sy = o.y - s->v0y[i], sz = o.z - s->v0z[i];
+        float u = ((sx * pvx + sy * pvy) + sz * pvz) * inv;
+        float qx = sy * e1z - sz * e1y;
+        float qy = sz * e1x - sx * e1z;
+        float qz = sx * e1y - sy * e1x;
+        float v = ((d.x * qx + d.y * qy) + d.z * qz) * inv;
+        float t = ((e2x * qx + e2y * qy) + e2z * qz) * inv;
+        int h = (det != 0.0f) & (u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) &
+                (t > tmin) & (t < tmax);
+        hit |= h;
+    }
+    return hit;
+}
+
+static int any_hit(const OScene* s, f3 o, f3 d, float tmin, float tmax) {
+    for (int64_t i0 = 0; i0 < s->n; i0 += CHUNK) {
+        int64_t i1 = i0 + CHUNK < s->n ? i0 + CHUNK : s->n;
+        if (any_hit_chunk(s, o, d, tmin, tmax, i0, i1)) return 1;
+    }
+    return 0;
+}
+
+/* per-triangle hit t as an order-preserving key (t > tmin >= 0 so t > 0):  */
+/* bits(t) for a hit, 0xFFFFFFFF for a miss                                   */
+static uint32_t min_key_chunk(const OScene* s, f3 o, f3 d, float tmin, float tmax, int64_t i0, int64_t i1) {
+    uint32_t best = 0xFFFFFFFFu;
+    for (int64_t i = i0; i < i1; i++) {
+        float e1x = s->e1x[i], e1y = s->e1y[i], e1z = s->e1z[i];
+        float e2x = s->e2x[i], e2y = s->e2y[i], e2z = s->e2z[i];
+        float pvx = d.y * e2z - d.z * e2y;
+        float pvy = d.z * e2x - d.x * e2z;
+        float pvz = d.x * e2y - d.y * e2x;
+        float det = (e1x * pvx + e1y * pvy) + e1z * pvz;
+        float inv = 1.0f / det;
+        float sx = o.x - s->v0x[i], sy = o.y - s->v0y[i], sz = o.z - s->v0z[i];
+        float u = ((sx * pvx + sy * pvy) + sz * pvz) * inv;
+        float qx = sy * e1z - sz * e1y;
+        float qy = sz * e1x - sx * e1z;
+        float qz = sx * e1y - sy * e1x;
+        float v = ((d.x * qx + d.y * qy) + d.z * qz) * inv;
+        float t = ((e2x * qx + e2y * qy) + e2z * qz) * inv;
+        int h = (det != 0.0f) & (u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) &
+                (t > tmin) & (t < tmax);
+        uint32_t tb;
+        memcpy(&tb, &t, 4);
+        uint32_t key = h ? tb : 0xFFFFFFFFu;
+        best = key < best ? key : best;
+    }
+    return best;
+}
+
+/* closest hit = lexicographic min of (t, original index) (O9, R15) */
+static int64_t closest_hit(const OScene* s, f3 o, f3 d, float tmin, float tmax, float* t_out) {
+    uint32_t best = 0xFFFFFFFFu;
+    int64_t best_chunk = -1;
+    for (int64_t i0 = 0; i0 < s->n; i0 += CHUNK) {
+        int64_t i1 = i0 + CHUNK < s->n ? i0 + CHUNK : s->n;
+        uint32_t k = min_key_chunk(s, o, d, tmin, tmax, i0, i1);
+        if (k < best) { best = k; best_chunk = i0; }
+    }
+    if (best_chunk < 0) return -1;
+    int64_t i1 = best_chunk + CHUNK < s->n ? best_chunk + CHUNK : s->n;
+    for (int64_t i = best_chunk; i < i1; i++)
+        if (min_key_chunk(s, o, d, tmin, tmax, i, i + 1) == best) {
+            memcpy(t_out, &best, 4);
+            return i;
+        }
+    return -1; /* unreachable */
+}
+
+/* unoccluded(a, b) (O9): segment shrunk by eps at both ends */
+static int occluded(const OScene* s, f3 a, f3 b) {
+    f3 d = sub(b, a);
+    float dist = sqrtf(dot(d, d));
+    f3 dir = mk(d.x / dist, d.y / dist, d.z / dist);
+    float tmin = s->eps, tmax = dist - s->eps;
+    if (!(tmax > tmin)) return 0;
+    return any_hit(s, a, dir, tmin, tmax);
+}
+
+/* exported single-query helpers (used by the pins) */
+int64_t oracle_closest_hit(const OScene* s, const float* o, const float* d, float tmin, float tmax, float* t) {
+    return closest_hit(s, ld3(o), ld3(d), tmin, tmax, t);
+}
+int oracle_occluded(const OScene* s, const float* a, const float* b) { return occluded(s, ld3(a), ld3(b)); }
+void oracle_occluded_batch(const OScene* s, const float* a, const float* b, int64_t n, uint8_t* out) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < n; i++) out[i] = (uint8_t)occluded(s, ld3(a + 3 * i), ld3(b + 3 * i));
+}
+void oracle_closest_batch(const OScene* s, const float* o, const float* d, int64_t n, float tmin, float tmax,
+                          int64_t* idx, float* t) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < n; i++) {
+        float tt = 0.0f;
+        idx[i] = closest_hit(s, ld3(o + 3 * i), ld3(d + 3 * i), tmin, tmax, &tt);
+        t[i] = tt;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* O2 — near/far classification: centroid strictly inside the view    */
+/* frustum AND closer than T.  cam = pos fwd up right tan_x tan_y.           */
+/* ------------------------------------------------------------------------ */
+void oracle_classify(const OScene* s, double T, uint8_t* labels, int64_t* n_near) {
+    const float* c = s->cam;
+    f3 pos = ld3(c), fwd = ld3(c + 3), up = ld3(c + 6), right = ld3(c + 9);
+    float tx = c[12], ty = c[13];
+    float T2 = (float)(T * T);
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < s->n; i++) {
+        f3 d = sub(ld3(s->cen + 3 * i), pos);
+        float z = dot(d, fwd), x = dot(d, right), y = dot(d, up);
+        int near = (z > 0.0f) && (fabsf(x) < z * tx) && (fabsf(y) < z * ty) && (dot(d, d) < T2);
+        labels[i] = (uint8_t)near;
+        cnt += near;
+    }
+    *n_near = cnt;
+}
+
+/* ------------------------------------------------------------------------ */
+/* VPL generation (P:44-65 near part; P:35, P:46 step 3 far part).           */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int64_t M, K_near, max_depth, rr, n_walks_fixed;
+    uint64_t seed;
+} OParams;
+
+typedef struct {
+    int64_t n_near, n_lit, K, M_far, n_walks, flags, n_far_tris, n_out;
+} OInfo;
+
+enum { FLAG_EMPTY_NEAR = 1, FLAG_EMPTY_FAR = 2, FLAG_WALK_BUDGET_UNMET = 4 };
+
+typedef struct {
+    float pos[3], nrm[3], flux[3];
+    int32_t tri, tag, depth, walk;
+} OVpl; /* tag 0 = near (patch), 1 = far (walk) */
+
+static inline f3 light_corner(const float* L) { return ld3(L); }
+static inline f3 light_eu(const float* L) { return ld3(L + 3); }
+static inline f3 light_ev(const float* L) { return ld3(L + 6); }
+static inline f3 light_n(const float* L) { return ld3(L + 9); }
+/* light centre = (corner + 0.5*e_u) + 0.5*e_v (O3) */
+static inline f3 light_centre(const float* L) {
+    return add(add(light_corner(L), scl(0.5f, light_eu(L))), scl(0.5f, light_ev(L)));
+}
+
+/* O3 — a near triangle is lit iff some light faces it, it faces the light,
+ * and the centroid -> light-centre segment is unoccluded (R6). */
+void oracle_lit(const OScene* s, const uint8_t* labels, uint8_t* lit) {
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t i = 0; i < s->n; i++) {
+        lit[i] = 0;
+        if (!labels[i]) continue;
+        f3 c = ld3(s->cen + 3 * i), n = ld3(s->nrm + 3 * i);
+        for (int l = 0; l < s->nL; l++) {
+            const float* L = s->lights + 16 * l;
+            f3 cl = light_centre(L);
+            if (dot(n, sub(cl, c)) > 0.0f && dot(light_n(L), sub(c, cl)) > 0.0f && !occluded(s, c, cl)) {
+                lit[i] = 1;
+                break;
+            }
+        }
+    }
+}
+
+/* O4 — 30-bit Morton code, bit i of qx -> 3i, qy -> 3i+1, qz -> 3i+2 */
+uint32_t oracle_morton3(uint32_t qx, uint32_t qy, uint32_t qz) {
+    uint32_t code = 0;
+    for (int b = 0; b < 10; b++) {
+        code |= ((qx >> b) & 1u) << (3 * b);
+        code |= ((qy >> b) & 1u) << (3 * b + 1);
+        code |= ((qz >> b) & 1u) << (3 * b + 2);
+    }
+    return code;
+}
+
+typedef struct { uint32_t code; int64_t idx; } MKey;
+static int mkey_cmp(const void* a, const void* b) {
+    const MKey *x = (const MKey*)a, *y = (const MKey*)b;
+    if (x->code != y->code) return x->code < y->code ? -1 : 1;
+    return x->idx < y->idx ? -1 : (x->idx > y->idx);
+}
+
+/* O4 + O5: order the lit-near set along the Morton curve and build
+ * the inclusive prefix f(i) of fixed-point areas.  Returns n_lit.    */
+int64_t oracle_near_table(const OScene* s, const uint8_t* lit, int64_t* order, uint64_t* P, uint32_t* codes) {
+    int64_t m = 0;
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = 0; i < s->n; i++)
+        if (lit[i]) {
+            m++;
+            for (int a = 0; a < 3; a++) {
+                float x = s->cen[3 * i + a];
+                if (x < lo[a]) lo[a] = x;
+                if (x > hi[a]) hi[a] = x;
+            }
+        }
+    if (m == 0) return 0;
+    float scale[3];
+    for (int a = 0; a < 3; a++) {
+        float ext = hi[a] - lo[a];
+        scale[a] = ext > 0.0f ? 1024.0f / ext : 0.0f;
+    }
+    MKey* keys = (MKey*)malloc(sizeof(MKey) * m);
+    int64_t k = 0;
+    for (int64_t i = 0; i < s->n; i++)
+        if (lit[i]) {
+            uint32_t q[3];
+            for (int a = 0; a < 3; a++) {
+                uint32_t qa = (uint32_t)((s->cen[3 * i + a] - lo[a]) * scale[a]);
+                q[a] = qa < 1023u ? qa : 1023u;
+            }
+            keys[k].code = oracle_morton3(q[0], q[1], q[2]);
+            keys[k].idx = i;
+            k++;
+        }
+    qsort(keys, m, sizeof(MKey), mkey_cmp);
+    uint64_t acc = 0;
+    for (int64_t j = 0; j < m; j++) {
+        order[j] = keys[j].idx;
+        if (codes) codes[j] = keys[j].code;
+        acc += s->aq[keys[j].idx];
+        P[j] = acc; /* f(j) = sum_{i<=j} s_i */
+    }
+    free(keys);
+    return m;
+}
+
+/* O6 — stratum k: s_k = floor((k*2^32 + x) * F / (K*2^32)), x = raw draw 0;
+ * j = g(s_k) = first index with P[j] > s_k.           */
+uint64_t oracle_stratum(uint64_t seed, int64_t k, int64_t K, uint64_t F) {
+    uint32_t x = oracle_draw(seed, STREAM_NEAR, (uint32_t)k, 0);
+    unsigned __int128 num = (((unsigned __int128)(uint64_t)k << 32) + x) * (unsigned __int128)F;
+    unsigned __int128 den = ((unsigned __int128)(uint64_t)K) << 32;
+    return (uint64_t)(num / den);
+}
+int64_t oracle_lookup_g(const uint64_t* P, int64_t m, uint64_t sk) {
+    int64_t j = 0; /* linear scan: the plain definition of g */
+    while (j < m && !(P[j] > sk)) j++;
+    return j;
+}
+
+/* O7 — uniform point in triangle via the square-root warp ([r10]). */
+static f3 point_in_tri(const OScene* s, int64_t t, float u1, float u2) {
+    const float* v = s->vert + 9 * t;
+    f3 v0 = ld3(v), v1 = ld3(v + 3), v2 = ld3(v + 6);
+    float su = sqrtf(u1);
+    float b1 = 1.0f - su;
+    float b2 = u2 * su;
+    float b0 = (1.0f - b1) - b2;
+    return add(add(scl(b1, v0), scl(b2, v1)), scl(b0, v2));
+}
+void oracle_point_in_tri(const OScene* s, int64_t t, float u1, float u2, float* p) {
+    f3 r = point_in_tri(s, t, u1, u2);
+    p[0] = r.x; p[1] = r.y; p[2] = r.z;
+}
+
+/* O8 — Eq. 2 for area lights (R1-R5): VPL flux =
+ * rho/pi * D * sum_l L_l * A_l cos_p cos_l / r^2 * V, D = f(N)/K.          */
+static void near_vpl(const OScene* s, const OParams* p, const int64_t* order, const uint64_t* P, int64_t m,
+                     int64_t K, float D, int64_t k, OVpl* out) {
+    uint64_t F = P[m - 1];
+    uint64_t sk = oracle_stratum(p->seed, k, K, F);
+    int64_t j = oracle_lookup_g(P, m, sk);
+    int64_t t = order[j];
+    float u1 = u01(oracle_draw(p->seed, STREAM_NEAR, (uint32_t)k, 1));
+    float u2 = u01(oracle_draw(p->seed, STREAM_NEAR, (uint32_t)k, 2));
+    f3 x = point_in_tri(s, t, u1, u2);
+    f3 n = ld3(s->nrm + 3 * t);
+    float E[3] = {0.0f, 0.0f, 0.0f};
+    for (int l = 0; l < s->nL; l++) {
+        const float* L = s->lights + 16 * l;
+        float u3 = u01(oracle_draw(p->seed, STREAM_NEAR, (uint32_t)k, 3 + 2 * l));
+        float u4 = u01(oracle_draw(p->seed, STREAM_NEAR, (uint32_t)k, 4 + 2 * l));
+        f3 y = add(add(light_corner(L), scl(u3, light_eu(L))), scl(u4, light_ev(L)));
+        f3 d = sub(y, x);
+        float r2 = dot(d, d);
+        float cp = dot(n, d);
+        float cl = -dot(light_n(L), d);
+        if (cp > 0.0f && cl > 0.0f && !occluded(s, x, y)) {
+            float g = ((L[12] * cp) * cl) / (r2 * r2);
+            for (int c = 0; c < 3; c++) E[c] += L[13 + c] * g;
+        }
+    }
+    const float INV_PI = (float)(1.0 / PI_D);
+    out->pos[0] = x.x; out->pos[1] = x.y; out->pos[2] = x.z;
+    out->nrm[0] = n.x; out->nrm[1] = n.y; out->nrm[2] = n.z;
+    for (int c = 0; c < 3; c++) out->flux[c] = (s->alb[3 * t + c] * (D * E[c])) * INV_PI;
+    out->tri = (int32_t)t; out->tag = 0; out->depth = 0; out->walk = (int32_t)k;
+}
+
+/* Malley cosine direction around unit n with the Duff et al. basis (O10). */
+static f3 malley(const OScene* s, uint64_t seed, uint32_t w, uint32_t* j, f3 n) {
+    (void)s;
+    float a = 0.0f, b = 0.0f, q = 0.0f;
+    int found = 0;
+    for (int att = 0; att < 64; att++) {
+        float ua = u01(oracle_draw(seed, STREAM_WALK, w, (*j)++));
+        float ub = u01(oracle_draw(seed, STREAM_WALK, w, (*j)++));
+        a = 2.0f * ua - 1.0f;
+        b = 2.0f * ub - 1.0f;
+        q = a * a + b * b;
+        if (q < 1.0f) { found = 1; break; }
+    }
+    if (!found) { a = 0.0f; b = 0.0f; q = 0.0f; }
+    float z = sqrtf(1.0f - q);
+    float sg = copysignf(1.0f, n.z);
+    float ia = -1.0f / (sg + n.z);
+    float bb = (n.x * n.y) * ia;
+    f3 t1 = mk(1.0f + sg * ((n.x * n.x) * ia), sg * bb, -sg * n.x);
+    f3 t2 = mk(bb, sg + (n.y * n.y) * ia, -n.y);
+    return mk((a * t1.x + b * t2.x) + z * n.x, (a * t1.y + b * t2.y) + z * n.y, (a * t1.z + b * t2.z) + z * n.z);
+}
+
+/* O10 — one sparse-IR walk (P:15, P:35, P:46 step 3; R9-R11).  Writes up to
+ * max_depth deposits (flux not yet divided by the walk count); returns count. */
+static int walk(const OScene* s, const OParams* p, const uint8_t* labels, uint32_t w, OVpl* dep) {
+    uint32_t j = 0;
+    uint32_t x0 = oracle_draw(p->seed, STREAM_WALK, w, j++);
+    int l = (int)(((uint64_t)x0 * (uint64_t)s->nL) >> 32);
+    const float* L = s->lights + 16 * l;
+    float beta[3];
+    for (int c = 0; c < 3; c++) beta[c] = (float)(PI_D * (double)L[12] * (double)L[13 + c] * (double)s->nL);
+    float u1 = u01(oracle_draw(p->seed, STREAM_WALK, w, j++));
+    float u2 = u01(oracle_draw(p->seed, STREAM_WALK, w, j++));
+    f3 o = add(add(light_corner(L), scl(u1, light_eu(L))), scl(u2, light_ev(L)));
+    f3 dir = malley(s, p->seed, w, &j, light_n(L));
+    const float INV_PI = (float)(1.0 / PI_D);
+    int cnt = 0;
+    for (int d = 1; d <= p->max_depth; d++) {
+        float t;
+        int64_t h = closest_hit(s, o, dir, s->eps, INFINITY, &t);
+        if (h < 0) break;
+        f3 nh = ld3(s->nrm + 3 * h);
+        if (dot(nh, dir) >= 0.0f) break; /* back face: absorbed */
+        f3 x = add(o, scl(t, dir));
+        const float* rho = s->alb + 3 * h;
+        if (!labels[h]) { /* far patch: deposit (near deposits discarded) */
+            OVpl* v = dep + cnt++;
+            v->pos[0] = x.x; v->pos[1] = x.y; v->pos[2] = x.z;
+            v->nrm[0] = nh.x; v->nrm[1] = nh.y; v->nrm[2] = nh.z;
+            for (int c = 0; c < 3; c++) v->flux[c] = (rho[c] * beta[c]) * INV_PI;
+            v->tri = (int32_t)h; v->tag = 1; v->depth = d; v->walk = (int32_t)w;
+        }
+        if (d == p->max_depth) break;
+        if (p->rr) {
+            float q = ((rho[0] + rho[1]) + rho[2]) / 3.0f;
+            float xi = u01(oracle_draw(p->seed, STREAM_WALK, w, j++));
+            if (!(xi < q)) break;
+            for (int c = 0; c < 3; c++) beta[c] = (beta[c] * rho[c]) / q;
+        } else {
+            for (int c = 0; c < 3; c++) beta[c] = beta[c] * rho[c];
+        }
+        dir = malley(s, p->seed, w, &j, nh);
+        o = x;
+    }
+    return cnt;
+}
+
+/* Full VPL generation (P:46 steps 1-3).  out must hold max_out records.
+ * Returns the number written (n_out) or -1 if max_out is too small.        */
+int64_t oracle_generate_vpls(const OScene* s, const uint8_t* labels, const OParams* p, OVpl* out,
+                             int64_t max_out, OInfo* info) {
+    memset(info, 0, sizeof(*info));
+    int64_t n_near = 0, n_far = 0;
+    for (int64_t i = 0; i < s->n; i++) {
+        n_near += labels[i] != 0;
+        n_far += labels[i] == 0;
+    }
+    info->n_near = n_near;
+    info->n_far_tris = n_far;
+    uint8_t* lit = (uint8_t*)malloc(s->n);
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (s->n + 1));
+    uint64_t* P = (uint64_t*)malloc(sizeof(uint64_t) * (s->n + 1));
+    int64_t m = 0;
+    if (p->K_near > 0 && p->n_walks_fixed == 0) {
+        oracle_lit(s, labels, lit);
+        m = oracle_near_table(s, lit, order, P, NULL);
+    }
+    info->n_lit = m;
+    int64_t K = p->K_near, Mf = p->M - p->K_near;
+    if (p->n_walks_fixed > 0) { K = 0; }
+    else if (m == 0) { K = 0; Mf = p->M; info->flags |= FLAG_EMPTY_NEAR; }
+    else if (n_far == 0) { K = p->M; Mf = 0; info->flags |= FLAG_EMPTY_FAR; }
+    if (K > max_out) { free(lit); free(order); free(P); return -1; }
+    info->K = K;
+    /* near part: K strata over [0, f(N)) */
+    if (K > 0) {
+        float D = (float)((double)P[m - 1] / (double)K / 1099511627776.0);
+#pragma omp parallel for schedule(dynamic, 8)
+        for (int64_t k = 0; k < K; k++) near_vpl(s, p, order, P, m, K, D, k, out + k);
+    }
+    /* far part: walks in index order, first-M_far-deposits rule (R11) */
+    int64_t n_out = K;
+    const int64_t B = 1024;
+    OVpl* buf = (OVpl*)malloc(sizeof(OVpl) * B * (p->max_depth > 0 ? p->max_depth : 1));
+    int* cnt = (int*)malloc(sizeof(int) * B);
+    int64_t walks = 0;
+    if (p->n_walks_fixed > 0) {
+        for (int64_t w0 = 0; w0 < p->n_walks_fixed; w0 += B) {
+            int64_t nb = p->n_walks_fixed - w0 < B ? p->n_walks_fixed - w0 : B;
+#pragma omp parallel for schedule(dynamic, 1)
+            for (int64_t i = 0; i < nb; i++) cnt[i] = walk(s, p, labels, (uint32_t)(w0 + i), buf + i * p->max_depth);
+            for (int64_t i = 0; i < nb; i++)
+                for (int c = 0; c < cnt[i]; c++) {
+                    if (n_out >= max_out) { free(buf); free(cnt); free(lit); free(order); free(P); return -1; }
+                    out[n_out++] = buf[i * p->max_depth + c];
+                }
+        }
+        walks = p->n_walks_fixed;
+    } else if (Mf > 0) {
+        if (K + Mf > max_out) { free(buf); free(cnt); free(lit); free(order); free(P); return -1; }
+        int64_t Wmax = 1024 * Mf, have = 0;
+        int done = 0;
+        for (int64_t w0 = 0; w0 < Wmax && !done; w0 += B) {
+            int64_t nb = Wmax - w0 < B ? Wmax - w0 : B;
+#pragma omp parallel for schedule(dynamic, 1)
+            for (int64_t i = 0; i < nb; i++) cnt[i] = walk(s, p, labels, (uint32_t)(w0 + i), buf + i * p->max_depth);
+            for (int64_t i = 0; i < nb && !done; i++) {
+                walks = w0 + i + 1;
+                for (int c = 0; c < cnt[i] && have < Mf; c++) { out[n_out++] = buf[i * p->max_depth + c]; have++; }
+                if (have >= Mf) done = 1;
+            }
+        }
+        if (!done) info->flags |= FLAG_WALK_BUDGET_UNMET;
+    }
+    /* divide walk fluxes by the number of walks used (R11) */
+    if (walks > 0) {
+        float fw = (float)walks;
+        for (int64_t i = K; i < n_out; i++)
+            for (int c = 0; c < 3; c++) out[i].flux[c] = out[i].flux[c] / fw;
+    }
+    info->M_far = n_out - K;
+    info->n_walks = walks;
+    info->n_out = n_out;
+    free(buf); free(cnt); free(lit); free(order); free(P);
+    return n_out;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O12 — G-buffer at the pixel centre (R16).  Output per pixel:     */
+/* gb[12] = pos(3) nrm(3) alb(3) t, tri (as float bits), front (0/1).        */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    float pos[3], nrm[3], alb[3], t;
+    int32_t tri, front;
+} OGbuf;
+
+static void primary_dir(const OScene* s, int px, int py, f3* dir_out) {
+    const float* c = s->cam;
+    f3 fwd = ld3(c + 3), up = ld3(c + 6), right = ld3(c + 9);
+    float tx = c[12], ty = c[13];
+    float sx = ((2.0f * ((float)px + 0.5f)) / (float)s->W - 1.0f) * tx;
+    float sy = (1.0f - (2.0f * ((float)py + 0.5f)) / (float)s->H) * ty;
+    f3 d = add(add(fwd, scl(sx, right)), scl(sy, up));
+    float len = sqrtf(dot(d, d));
+    *dir_out = mk(d.x / len, d.y / len, d.z / len);
+}
+
+void oracle_gbuffer(const OScene* s, const int32_t* pix, int64_t n_pix, OGbuf* out) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t k = 0; k < n_pix; k++) {
+        int32_t id = pix[k];
+        int px = id % s->W, py = id / s->W;
+        f3 dir;
+        primary_dir(s, px, py, &dir);
+        f3 o = ld3(s->cam);
+        float t = 0.0f;
+        int64_t h = closest_hit(s, o, dir, 0.0f, INFINITY, &t);
+        OGbuf* g = out + k;
+        memset(g, 0, sizeof(*g));
+        g->tri = -1;
+        if (h < 0) continue;
+        f3 x = add(o, scl(t, dir));
+        f3 n = ld3(s->nrm + 3 * h);
+        g->pos[0] = x.x; g->pos[1] = x.y; g->pos[2] = x.z;
+        g->nrm[0] = n.x; g->nrm[1] = n.y; g->nrm[2] = n.z;
+        for (int c = 0; c < 3; c++) g->alb[c] = s->alb[3 * h + c];
+        g->t = t;
+        g->tri = (int32_t)h;
+        g->front = dot(n, dir) < 0.0f;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* O13 — the gather, Eq. 1 indirect term, brute-force visibility:  */
+/* L(x) = rho_x/pi * sum_i Phi_i cx ci / (r2 * max(r2, b^2)) * V(x, y_i),     */
+/* cx = n_x.d, ci = -n_i.d, d = y_i - x; self-triangle excluded (R14);        */
+/* accumulated in fp64 in VPL array order.                                    */
+/* Optional per-pixel bitmaps (ceil(M/32) words each): traced (cull passed)  */
+/* and visible.                                                               */
+/* ------------------------------------------------------------------------ */
+void oracle_gather(const OScene* s, const OGbuf* gb, int64_t n_pix, const OVpl* v, int64_t M, float* rgb,
+                   double* rgb64, int64_t* traced_count, uint32_t* traced_bits, uint32_t* vis_bits) {
+    int64_t words = (M + 31) / 32;
+    int64_t total_traced = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : total_traced)
+    for (int64_t k = 0; k < n_pix; k++) {
+        const OGbuf* g = gb + k;
+        double acc[3] = {0.0, 0.0, 0.0};
+        if (traced_bits) memset(traced_bits + k * words, 0, sizeof(uint32_t) * words);
+        if (vis_bits) memset(vis_bits + k * words, 0, sizeof(uint32_t) * words);
+        if (g->tri >= 0 && g->front) {
+            f3 x = ld3(g->pos), nx = ld3(g->nrm);
+            for (int64_t i = 0; i < M; i++) {
+                if (v[i].tri == g->tri) continue;
+                f3 y = ld3(v[i].pos);
+                f3 d = sub(y, x);
+                float r2 = dot(d, d);
+                float cx = dot(nx, d);
+                float ci = -dot(ld3(v[i].nrm), d);
+                if (!(cx > 0.0f && ci > 0.0f)) continue;
+                total_traced++;
+                if (traced_bits) traced_bits[k * words + i / 32] |= 1u << (i % 32);
+                if (occluded(s, x, y)) continue;
+                if (vis_bits) vis_bits[k * words + i / 32] |= 1u << (i % 32);
+                double r2d = (double)r2, b2d = (double)s->b2;
+                double G = ((double)cx * (double)ci) / (r2d * (r2d > b2d ? r2d : b2d));
+                for (int c = 0; c < 3; c++) acc[c] += (double)v[i].flux[c] * G;
+            }
+        }
+        for (int c = 0; c < 3; c++) {
+            double val = acc[c] * (double)g->alb[c] / PI_D;
+            if (!(g->tri >= 0 && g->front)) val = 0.0;
+            rgb[3 * k + c] = (float)val;
+            if (rgb64) rgb64[3 * k + c] = val;
+        }
+    }
+    if (traced_count) *traced_count = total_traced;
+}
+
+/* visibility of explicit (point, VPL) pairs — for sampled-pair parity */
+void oracle_pair_visibility(const OScene* s, const float* x, const float* y, int64_t n, uint8_t* vis) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < n; i++) vis[i] = (uint8_t)!occluded(s, ld3(x + 3 * i), ld3(y + 3 * i));
+}
+
+int oracle_abi(void) { return ORACLE_ABI; }
+int oracle_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
