@@ -1,0 +1,341 @@
+// common.cuh — device-side layouts, exact fp32 helpers, Philox and BVH
+// traversal shared by the kernels of libvplgi.so (sm_100a).
+//
+// Every translation unit is compiled with -fmad=false: a*b+c stays an FMUL
+// followed by an FADD, so the bit-exact steps (DESIGN.md §3 O1-O12) match the
+// IEEE definition written in DESIGN.md.  Where a result only has to be
+// conservative (the BVH slab test) the code calls fmaf() explicitly.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+
+#include "../../include/vplgi.h"
+
+namespace vplgi {
+
+// ------------------------------------------------------------------ errors
+void set_error(const char* fmt, ...);
+int32_t check_cuda(cudaError_t e, const char* what);
+int32_t check_launch(const char* what);  // also counts the launch (vpl_launch_count)
+int32_t check_arch();
+
+#define VPL_TRY(expr)                      \
+    do {                                   \
+        int32_t _st = (expr);              \
+        if (_st != VPL_OK) return _st;     \
+    } while (0)
+#define VPL_CUDA(call) VPL_TRY(::vplgi::check_cuda((call), #call))
+#define VPL_LAUNCHED(name) VPL_TRY(::vplgi::check_launch(name))
+
+// ------------------------------------------------------------------ layouts
+constexpr int kMaxLights = VPL_MAX_LIGHTS;
+constexpr size_t kAlign = 256;
+__host__ __device__ inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+// Scene blob = SceneHdr followed by SoA arrays (offsets from the blob start).
+struct SceneHdr {
+    int64_t n;
+    int32_t nL, W, H, pad0;
+    float cam[14];                  // pos fwd up right tan_x tan_y
+    float lights[16 * kMaxLights];  // vpl_light rows
+    uint32_t bbox_enc[6];           // order-preserving encodings (lo x y z, hi x y z) for atomics
+    float bbox_lo[3], bbox_hi[3];
+    double diag;
+    float eps, b2, box_pad, pad1;
+    unsigned long long bad;         // lowest degenerate triangle (ULLONG_MAX = none)
+    int64_t off_verts, off_nrm, off_alb, off_cen, off_aq;
+};
+
+struct SceneView {
+    const SceneHdr* hdr;
+    const float* verts;     // [9N]
+    const float4* nrm;      // [N] xyz = unit normal, w = area
+    const float4* alb;      // [N] rgb albedo
+    const float4* cen;      // [N] centroid
+    const uint64_t* aq;     // [N] 40-bit fixed-point area
+};
+
+inline size_t scene_layout(int64_t n, SceneHdr* h) {
+    size_t off = align_up(sizeof(SceneHdr));
+    size_t o_v = off; off = align_up(off + sizeof(float) * 9 * (size_t)n);
+    size_t o_n = off; off = align_up(off + sizeof(float4) * (size_t)n);
+    size_t o_a = off; off = align_up(off + sizeof(float4) * (size_t)n);
+    size_t o_c = off; off = align_up(off + sizeof(float4) * (size_t)n);
+    size_t o_q = off; off = align_up(off + sizeof(uint64_t) * (size_t)n);
+    if (h) { h->off_verts = o_v; h->off_nrm = o_n; h->off_alb = o_a; h->off_cen = o_c; h->off_aq = o_q; }
+    return off;
+}
+
+// Host-side view: offsets are read from a host copy of the header.
+inline SceneView scene_view(const void* blob, int64_t n) {
+    SceneHdr h;
+    scene_layout(n, &h);
+    const char* b = (const char*)blob;
+    SceneView v;
+    v.hdr = (const SceneHdr*)b;
+    v.verts = (const float*)(b + h.off_verts);
+    v.nrm = (const float4*)(b + h.off_nrm);
+    v.alb = (const float4*)(b + h.off_alb);
+    v.cen = (const float4*)(b + h.off_cen);
+    v.aq = (const uint64_t*)(b + h.off_aq);
+    return v;
+}
+
+// BVH blob = BvhHdr, internal nodes (4 float4 each), leaf-ordered triangles
+// (3 float4 each: v0 | orig index bits, e1, e2).
+struct BvhHdr {
+    int64_t n;
+    int32_t root;       // 0 (internal) or ~0 (single leaf)
+    int32_t pad;
+    int64_t off_nodes, off_tris;
+};
+struct BvhView {
+    const float4* nodes;
+    const float4* tris;
+    int32_t root;
+};
+inline size_t bvh_layout(int64_t n, BvhHdr* h) {
+    size_t off = align_up(sizeof(BvhHdr));
+    size_t o_n = off; off = align_up(off + sizeof(float4) * 4 * (size_t)(n > 1 ? n - 1 : 1));
+    size_t o_t = off; off = align_up(off + sizeof(float4) * 3 * (size_t)n);
+    if (h) { h->n = n; h->root = n > 1 ? 0 : ~0; h->off_nodes = o_n; h->off_tris = o_t; }
+    return off;
+}
+inline BvhView bvh_view(const void* blob, int64_t n) {
+    BvhHdr h;
+    bvh_layout(n, &h);
+    BvhView v;
+    v.nodes = (const float4*)((const char*)blob + h.off_nodes);
+    v.tris = (const float4*)((const char*)blob + h.off_tris);
+    v.root = h.root;
+    return v;
+}
+
+// stream-ordered host copy of the scene header (n, offsets, constants)
+inline int32_t read_scene_hdr(const void* d_scene, cudaStream_t s, SceneHdr* out) {
+    VPL_CUDA(cudaMemcpyAsync(out, d_scene, sizeof(SceneHdr), cudaMemcpyDeviceToHost, s));
+    VPL_CUDA(cudaStreamSynchronize(s));
+    return VPL_OK;
+}
+
+// bump allocator over a caller work buffer (base may be null for sizing)
+struct Bump {
+    char* base;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t count) {
+        T* p = base ? (T*)(base + off) : nullptr;
+        off = align_up(off + sizeof(T) * count);
+        return p;
+    }
+};
+
+// ------------------------------------------------------------------ fp32 vector math (exact op order, O0)
+struct f3 { float x, y, z; };
+__device__ __forceinline__ f3 mk3(float x, float y, float z) { return f3{x, y, z}; }
+__device__ __forceinline__ f3 ld3(const float* p) { return f3{p[0], p[1], p[2]}; }
+__device__ __forceinline__ f3 xyz(float4 a) { return f3{a.x, a.y, a.z}; }
+__device__ __forceinline__ f3 operator+(f3 a, f3 b) { return f3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ f3 operator-(f3 a, f3 b) { return f3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ f3 operator*(float s, f3 a) { return f3{s * a.x, s * a.y, s * a.z}; }
+__device__ __forceinline__ float dot(f3 a, f3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+__device__ __forceinline__ f3 cross(f3 a, f3 b) {
+    return f3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+
+// ------------------------------------------------------------------ Philox4x32-10
+struct Philox {
+    // counter = (j >> 2, item, stream, 0), key = (seed lo, seed hi); draw j = lane j & 3
+    uint32_t item, stream, k0, k1;
+    uint32_t j = 0;
+    uint32_t blk_id = 0xFFFFFFFFu;
+    uint32_t blk[4];
+    __device__ Philox(uint64_t seed, uint32_t stream_, uint32_t item_)
+        : item(item_), stream(stream_), k0((uint32_t)seed), k1((uint32_t)(seed >> 32)) {}
+    __device__ static void block(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1,
+                                 uint32_t out[4]) {
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+            uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+            uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+            uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+            c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        }
+        out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+    }
+    __device__ uint32_t at(uint32_t jj) {
+        uint32_t b = jj >> 2;
+        if (b != blk_id) { block(b, item, stream, 0u, k0, k1, blk); blk_id = b; }
+        return blk[jj & 3u];
+    }
+    __device__ uint32_t next() { return at(j++); }
+};
+__device__ __forceinline__ float u01(uint32_t x) { return (float)(x >> 8) * 0x1p-24f; }
+
+// ------------------------------------------------------------------ ray / box / triangle
+struct Ray {
+    f3 o, d;           // origin, direction (not necessarily unit)
+    f3 idir, ood;      // 1/d (zero components nudged) and o * idir, for the slab test only
+    float tmin, tmax;
+};
+__device__ __forceinline__ float nudge(float x) { return fabsf(x) < 1e-30f ? copysignf(1e-30f, x) : x; }
+__device__ __forceinline__ Ray make_ray(f3 o, f3 d, float tmin, float tmax) {
+    Ray r;
+    r.o = o; r.d = d; r.tmin = tmin; r.tmax = tmax;
+    r.idir = mk3(1.0f / nudge(d.x), 1.0f / nudge(d.y), 1.0f / nudge(d.z));
+    r.ood = mk3(o.x * r.idir.x, o.y * r.idir.y, o.z * r.idir.z);
+    return r;
+}
+
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// Conservative slab test (boxes are padded at build time).
+__device__ __forceinline__ bool slab(const Ray& r, float lox, float hix, float loy, float hiy, float loz,
+                                     float hiz, float tlimit, float& tnear) {
+    float tx0 = fmaf(lox, r.idir.x, -r.ood.x), tx1 = fmaf(hix, r.idir.x, -r.ood.x);
+    float ty0 = fmaf(loy, r.idir.y, -r.ood.y), ty1 = fmaf(hiy, r.idir.y, -r.ood.y);
+    float tz0 = fmaf(loz, r.idir.z, -r.ood.z), tz1 = fmaf(hiz, r.idir.z, -r.ood.z);
+    float tn = fmax3(fminf(tx0, tx1), fminf(ty0, ty1), fmaxf(fminf(tz0, tz1), r.tmin));
+    float tf = fmin3(fmaxf(tx0, tx1), fmaxf(ty0, ty1), fminf(fmaxf(tz0, tz1), tlimit));
+    tnear = tn;
+    return tn <= tf;
+}
+
+// Moller-Trumbore exactly as DESIGN.md §3 O9 (no FMA: -fmad=false TU).
+__device__ __forceinline__ bool mt_hit(f3 o, f3 d, float4 a, float4 b, float4 c, float tmin, float tmax, float& t) {
+    f3 v0 = xyz(a), e1 = xyz(b), e2 = xyz(c);
+    f3 pv = cross(d, e2);
+    float det = dot(e1, pv);
+    float inv = 1.0f / det;
+    f3 s = o - v0;
+    float u = dot(s, pv) * inv;
+    f3 q = cross(s, e1);
+    float v = dot(d, q) * inv;
+    t = dot(e2, q) * inv;
+    return (det != 0.0f) & (u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) & (t > tmin) & (t < tmax);
+}
+
+struct TravStats {
+    uint32_t boxes = 0, tris = 0;
+};
+
+constexpr int kStack = 96;
+
+// Any hit in (tmin, tmax): true if some triangle's MT hit lies inside.
+template <bool kCount>
+__device__ __forceinline__ bool bvh_any_hit(const BvhView& bv, const Ray& r, TravStats* st) {
+    int stack[kStack];
+    int sp = 0;
+    int node = bv.root;
+    while (true) {
+        if (node >= 0) {
+            const float4* nd = bv.nodes + 4 * node;
+            float4 n0 = __ldg(nd + 0), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
+            float t0, t1;
+            bool h0 = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, r.tmax, t0);
+            bool h1 = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, r.tmax, t1);
+            if (kCount) st->boxes += 2;
+            int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
+            if (h0 && h1) {
+                bool first0 = t0 <= t1;
+                if (sp < kStack) stack[sp++] = first0 ? c1 : c0;
+                node = first0 ? c0 : c1;
+                continue;
+            }
+            if (h0) { node = c0; continue; }
+            if (h1) { node = c1; continue; }
+        } else {
+            int p = ~node;
+            const float4* tr = bv.tris + 3 * p;
+            float t;
+            if (kCount) st->tris += 1;
+            if (mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t)) return true;
+        }
+        if (sp == 0) return false;
+        node = stack[--sp];
+    }
+}
+
+// Closest hit in (tmin, tmax): lexicographic min of (t, original index) (O9, R15).
+__device__ __forceinline__ int bvh_closest(const BvhView& bv, const Ray& r, float& t_best) {
+    int stack[kStack];
+    int sp = 0;
+    int node = bv.root;
+    int best = -1;
+    float tb = r.tmax;
+    t_best = r.tmax;
+    while (true) {
+        if (node >= 0) {
+            const float4* nd = bv.nodes + 4 * node;
+            float4 n0 = __ldg(nd + 0), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
+            float t0, t1;
+            // ties at t == t_best must still be explored (lowest index wins): tnear <= tb
+            bool h0 = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tb, t0);
+            bool h1 = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tb, t1);
+            int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
+            if (h0 && h1) {
+                bool first0 = t0 <= t1;
+                if (sp < kStack) stack[sp++] = first0 ? c1 : c0;
+                node = first0 ? c0 : c1;
+                continue;
+            }
+            if (h0) { node = c0; continue; }
+            if (h1) { node = c1; continue; }
+        } else {
+            int p = ~node;
+            const float4* tr = bv.tris + 3 * p;
+            float4 a = __ldg(tr);
+            float t;
+            // hit test against the ORIGINAL (tmin, tmax); order against the best so far
+            if (mt_hit(r.o, r.d, a, __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t)) {
+                int orig = __float_as_int(a.w);
+                if (t < tb || (t == tb && orig < best)) { tb = t; best = orig; }
+            }
+        }
+        if (sp == 0) break;
+        node = stack[--sp];
+    }
+    t_best = tb;
+    return best;
+}
+
+// unoccluded(a, b) with the eps-shrunk segment (O9)
+template <bool kCount>
+__device__ __forceinline__ bool segment_occluded(const BvhView& bv, f3 a, f3 b, float eps, TravStats* st) {
+    f3 d = b - a;
+    float dist = sqrtf(dot(d, d));
+    f3 dir = mk3(d.x / dist, d.y / dist, d.z / dist);
+    float tmin = eps, tmax = dist - eps;
+    if (!(tmax > tmin)) return false;
+    Ray r = make_ray(a, dir, tmin, tmax);
+    return bvh_any_hit<kCount>(bv, r, st);
+}
+
+// tile -> pixel mapping: warp w of a call covers an 8x4 block
+struct TileMap {
+    const int32_t* tiles;
+    int32_t n_tiles, tw, th, W, H, tiles_x, blocks_per_tile, bx_per_tile;
+    __host__ __device__ int64_t n_warps() const { return (int64_t)n_tiles * blocks_per_tile; }
+    // returns the pixel of (warp g, lane) or -1 when outside the image
+    __device__ __forceinline__ int32_t pixel(int64_t g, int lane) const {
+        int32_t ti = (int32_t)(g / blocks_per_tile), sub = (int32_t)(g % blocks_per_tile);
+        int32_t t = tiles[ti];
+        int32_t tx = t % tiles_x, ty = t / tiles_x;
+        int32_t x = tx * tw + (sub % bx_per_tile) * 8 + (lane & 7);
+        int32_t y = ty * th + (sub / bx_per_tile) * 4 + (lane >> 3);
+        return (x < W && y < H) ? y * W + x : -1;
+    }
+};
+
+}  // namespace vplgi

@@ -1,0 +1,320 @@
+// render.cu — a7 render_gbuffer (O12), a8 gather_indirect (Eq. 1, O13) and
+// the test hooks that share their traversal code.
+#include "common.cuh"
+
+namespace vplgi {
+
+constexpr double kPiR = 3.14159265358979323846;
+
+// O12 — centre-sample pinhole ray, closest hit
+__global__ void k_gbuffer(SceneView sv, BvhView bv, TileMap tm, vpl_gpoint* __restrict__ gb) {
+    int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (g >= tm.n_warps()) return;
+    int32_t pix = tm.pixel(g, lane);
+    if (pix < 0) return;
+    const SceneHdr* h = sv.hdr;
+    const float* c = h->cam;
+    int px = pix % h->W, py = pix / h->W;
+    f3 pos = ld3(c), fwd = ld3(c + 3), up = ld3(c + 6), right = ld3(c + 9);
+    float sx = ((2.0f * ((float)px + 0.5f)) / (float)h->W - 1.0f) * c[12];
+    float sy = (1.0f - (2.0f * ((float)py + 0.5f)) / (float)h->H) * c[13];
+    f3 d = (fwd + sx * right) + sy * up;
+    float len = sqrtf(dot(d, d));
+    f3 dir = mk3(d.x / len, d.y / len, d.z / len);
+    Ray r = make_ray(pos, dir, 0.0f, __int_as_float(0x7f800000));
+    float t;
+    int hit = bvh_closest(bv, r, t);
+    vpl_gpoint o;
+    if (hit < 0) {
+        o.pos[0] = o.pos[1] = o.pos[2] = 0.0f;
+        o.nrm[0] = o.nrm[1] = o.nrm[2] = 0.0f;
+        o.alb[0] = o.alb[1] = o.alb[2] = 0.0f;
+        o.tri = -1; o.front = 0; o.t = 0.0f;
+    } else {
+        f3 x = pos + t * dir;
+        float4 n = sv.nrm[hit];
+        float4 a = sv.alb[hit];
+        o.pos[0] = x.x; o.pos[1] = x.y; o.pos[2] = x.z;
+        o.nrm[0] = n.x; o.nrm[1] = n.y; o.nrm[2] = n.z;
+        o.alb[0] = a.x; o.alb[1] = a.y; o.alb[2] = a.z;
+        o.tri = hit; o.t = t;
+        o.front = dot(xyz(n), dir) < 0.0f;
+    }
+    gb[pix] = o;
+}
+
+struct VplGeo {
+    f3 y, n, phi;
+    int tri;
+};
+__device__ __forceinline__ VplGeo load_vpl(const vpl_record* v) {
+    const float4* p = (const float4*)v;
+    float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+    VplGeo g;
+    g.y = xyz(a); g.tri = __float_as_int(a.w);
+    g.n = xyz(b); g.phi = xyz(c);
+    return g;
+}
+
+// a8 — Eq. 1 gather.  One warp per 8x4 pixel block; all lanes walk
+// the VPL list in the same order, so the shadow rays of a warp share their
+// end point (coherent traversal).  fp32 two-level accumulation: a per-batch
+// partial is folded into the running total every 256 VPLs.
+template <bool kCount>
+__global__ void __launch_bounds__(128) k_gather(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb,
+                                                const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
+                                                vpl_counters* __restrict__ ctr, int* __restrict__ queue) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = tm.n_warps();
+    const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
+    while (true) {
+        int64_t g;
+        if (lane == 0) g = atomicAdd(queue, 1);
+        g = __shfl_sync(0xFFFFFFFFu, g, 0);
+        if (g >= nw) break;
+        int32_t pix = tm.pixel(g, lane);
+        bool active = false;
+        f3 x = mk3(0, 0, 0), nx = mk3(0, 0, 0), rho = mk3(0, 0, 0);
+        int tri_x = -1;
+        if (pix >= 0) {
+            const float4* gp = (const float4*)(gb + pix);
+            float4 a = gp[0], b = gp[1], c = gp[2];
+            tri_x = __float_as_int(a.w);
+            active = tri_x >= 0 && __float_as_int(b.w) != 0;
+            x = xyz(a); nx = xyz(b); rho = xyz(c);
+        }
+        float acc[3] = {0.0f, 0.0f, 0.0f};
+        TravStats st;
+        unsigned long long n_traced = 0, n_vis = 0;
+        if (__any_sync(0xFFFFFFFFu, active)) {
+            for (int i0 = 0; i0 < M; i0 += 256) {
+                float part[3] = {0.0f, 0.0f, 0.0f};
+                int i1 = min(M, i0 + 256);
+                for (int i = i0; i < i1; ++i) {
+                    VplGeo v = load_vpl(vpls + i);
+                    if (!active || v.tri == tri_x) continue;
+                    f3 d = v.y - x;
+                    float r2 = dot(d, d);
+                    float cx = dot(nx, d);
+                    float ci = -dot(v.n, d);
+                    if (!(cx > 0.0f && ci > 0.0f)) continue;
+                    if (kCount) ++n_traced;
+                    if (segment_occluded<kCount>(bv, x, v.y, eps, &st)) continue;
+                    if (kCount) ++n_vis;
+                    float w = __fdividef(cx * ci, r2 * fmaxf(r2, b2));
+                    part[0] = fmaf(v.phi.x, w, part[0]);
+                    part[1] = fmaf(v.phi.y, w, part[1]);
+                    part[2] = fmaf(v.phi.z, w, part[2]);
+                }
+                acc[0] += part[0]; acc[1] += part[1]; acc[2] += part[2];
+            }
+        }
+        if (pix >= 0) {
+            const float s = (float)(1.0 / kPiR);
+            float* o = rgb + 3 * (int64_t)pix;
+            o[0] = active ? acc[0] * rho.x * s : 0.0f;
+            o[1] = active ? acc[1] * rho.y * s : 0.0f;
+            o[2] = active ? acc[2] * rho.z * s : 0.0f;
+        }
+        if (kCount) {
+            unsigned long long pairs = active ? (unsigned long long)M : 0ull;
+            unsigned long long bx = st.boxes, tt = st.tris;
+            for (int o = 16; o > 0; o >>= 1) {
+                pairs += __shfl_xor_sync(0xFFFFFFFFu, pairs, o);
+                n_traced += __shfl_xor_sync(0xFFFFFFFFu, n_traced, o);
+                n_vis += __shfl_xor_sync(0xFFFFFFFFu, n_vis, o);
+                bx += __shfl_xor_sync(0xFFFFFFFFu, bx, o);
+                tt += __shfl_xor_sync(0xFFFFFFFFu, tt, o);
+            }
+            if (lane == 0) {
+                atomicAdd(&ctr->pairs, pairs);
+                atomicAdd(&ctr->traced, n_traced);
+                atomicAdd(&ctr->visible, n_vis);
+                atomicAdd(&ctr->box_tests, bx);
+                atomicAdd(&ctr->tri_tests, tt);
+            }
+        }
+    }
+}
+
+// test hook: traced / visible bits of listed pixels x all VPLs (same code path)
+__global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict__ gb, const vpl_record* __restrict__ vpls,
+                          int32_t M, const int32_t* __restrict__ pixels, int32_t n_px, uint32_t* __restrict__ tbits,
+                          uint32_t* __restrict__ vbits) {
+    int64_t words = (M + 31) / 32;
+    int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (id >= (int64_t)n_px * words) return;
+    int32_t k = (int32_t)(id / words), wd = (int32_t)(id % words);
+    const vpl_gpoint* g = gb + pixels[k];
+    uint32_t tb = 0, vb = 0;
+    if (g->tri >= 0 && g->front) {
+        f3 x = ld3(g->pos), nx = ld3(g->nrm);
+        for (int b = 0; b < 32; ++b) {
+            int i = wd * 32 + b;
+            if (i >= M) break;
+            VplGeo v = load_vpl(vpls + i);
+            if (v.tri == g->tri) continue;
+            f3 d = v.y - x;
+            float cx = dot(nx, d);
+            float ci = -dot(v.n, d);
+            if (!(cx > 0.0f && ci > 0.0f)) continue;
+            tb |= 1u << b;
+            if (!segment_occluded<false>(bv, x, v.y, sv.hdr->eps, nullptr)) vb |= 1u << b;
+        }
+    }
+    tbits[id] = tb;
+    vbits[id] = vb;
+}
+
+__global__ void k_closest_batch(BvhView bv, const float* __restrict__ o, const float* __restrict__ d, int64_t n,
+                                float tmin, float tmax, int32_t* __restrict__ tri, float* __restrict__ tout) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Ray r = make_ray(ld3(o + 3 * i), ld3(d + 3 * i), tmin, tmax);
+    float t;
+    int h = bvh_closest(bv, r, t);
+    tri[i] = h;
+    tout[i] = h >= 0 ? t : 0.0f;
+}
+
+__global__ void k_occluded_batch(SceneView sv, BvhView bv, const float* __restrict__ a, const float* __restrict__ b,
+                                 int64_t n, uint8_t* __restrict__ occ) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    occ[i] = segment_occluded<false>(bv, ld3(a + 3 * i), ld3(b + 3 * i), sv.hdr->eps, nullptr);
+}
+
+__global__ void k_philox_batch(const uint32_t* __restrict__ in, int64_t n, uint32_t* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t* c = in + 6 * i;
+    uint32_t r[4];
+    Philox::block(c[0], c[1], c[2], c[3], c[4], c[5], r);
+    for (int k = 0; k < 4; ++k) out[4 * i + k] = r[k];
+}
+
+static inline int nb(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+static int32_t make_tilemap(const SceneHdr& hh, const int32_t* d_tiles, int32_t n_tiles, int32_t tw, int32_t th,
+                            TileMap* tm) {
+    if (!d_tiles || n_tiles < 0 || tw <= 0 || th <= 0 || tw % 8 || th % 4) {
+        set_error("bad tile arguments (tile_w %% 8 == 0, tile_h %% 4 == 0 required)");
+        return VPL_EINVAL;
+    }
+    tm->tiles = d_tiles;
+    tm->n_tiles = n_tiles;
+    tm->tw = tw; tm->th = th;
+    tm->W = hh.W; tm->H = hh.H;
+    tm->tiles_x = (hh.W + tw - 1) / tw;
+    tm->bx_per_tile = tw / 8;
+    tm->blocks_per_tile = (tw / 8) * (th / 4);
+    return VPL_OK;
+}
+
+}  // namespace vplgi
+
+using namespace vplgi;
+
+extern "C" {
+
+int32_t vpl_render_gbuffer(const void* d_scene, const void* d_bvh, const int32_t* d_tiles, int32_t n_tiles,
+                           int32_t tile_w, int32_t tile_h, vpl_gpoint* d_gbuf, void* stream) {
+    if (!d_scene || !d_bvh || !d_gbuf) { set_error("vpl_render_gbuffer: null pointer"); return VPL_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    SceneHdr hh;
+    VPL_TRY(read_scene_hdr(d_scene, s, &hh));
+    TileMap tm;
+    VPL_TRY(make_tilemap(hh, d_tiles, n_tiles, tile_w, tile_h, &tm));
+    if (n_tiles == 0) return VPL_OK;
+    int64_t threads = tm.n_warps() * 32;
+    k_gbuffer<<<nb(threads, 128), 128, 0, s>>>(scene_view(d_scene, hh.n), bvh_view(d_bvh, hh.n), tm, d_gbuf);
+    VPL_LAUNCHED("k_gbuffer");
+    return VPL_OK;
+}
+
+int32_t vpl_gather_bytes(size_t* work_bytes) {
+    if (!work_bytes) return VPL_EINVAL;
+    *work_bytes = 256;
+    return VPL_OK;
+}
+
+int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf, const vpl_record* d_vpls,
+                            int32_t n_vpls, const int32_t* d_tiles, int32_t n_tiles, int32_t tile_w, int32_t tile_h,
+                            float* d_rgb, vpl_counters* d_ctr, void* d_work, size_t work_bytes, void* stream) {
+    if (!d_scene || !d_bvh || !d_gbuf || !d_rgb || !d_work || n_vpls < 0 || (n_vpls > 0 && !d_vpls)) {
+        set_error("vpl_gather_indirect: bad arguments");
+        return VPL_EINVAL;
+    }
+    if (work_bytes < 256) { set_error("vpl_gather_indirect: work too small"); return VPL_ESMALL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    SceneHdr hh;
+    VPL_TRY(read_scene_hdr(d_scene, s, &hh));
+    TileMap tm;
+    VPL_TRY(make_tilemap(hh, d_tiles, n_tiles, tile_w, tile_h, &tm));
+    if (n_tiles == 0) return VPL_OK;
+    int* queue = (int*)d_work;
+    VPL_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
+    int dev = 0, sms = 148;
+    VPL_CUDA(cudaGetDevice(&dev));
+    VPL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int grid = sms * 8;  // persistent: 8 CTAs x 4 warps per SM
+    SceneView sv = scene_view(d_scene, hh.n);
+    BvhView bv = bvh_view(d_bvh, hh.n);
+    if (d_ctr)
+        k_gather<true><<<grid, 128, 0, s>>>(sv, bv, tm, d_gbuf, d_vpls, n_vpls, d_rgb, d_ctr, queue);
+    else
+        k_gather<false><<<grid, 128, 0, s>>>(sv, bv, tm, d_gbuf, d_vpls, n_vpls, d_rgb, nullptr, queue);
+    VPL_LAUNCHED("k_gather");
+    return VPL_OK;
+}
+
+int32_t vpl_visibility_dump(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf, const vpl_record* d_vpls,
+                            int32_t n_vpls, const int32_t* d_pixels, int32_t n_pixels, uint32_t* d_traced_bits,
+                            uint32_t* d_vis_bits, void* stream) {
+    if (!d_scene || !d_bvh || !d_gbuf || !d_pixels || !d_traced_bits || !d_vis_bits || n_vpls <= 0 || n_pixels < 0)
+        return VPL_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    SceneHdr hh;
+    VPL_TRY(read_scene_hdr(d_scene, s, &hh));
+    int64_t total = (int64_t)n_pixels * ((n_vpls + 31) / 32);
+    if (total == 0) return VPL_OK;
+    k_visdump<<<nb(total, 64), 64, 0, s>>>(scene_view(d_scene, hh.n), bvh_view(d_bvh, hh.n), d_gbuf, d_vpls, n_vpls,
+                                           d_pixels, n_pixels, d_traced_bits, d_vis_bits);
+    VPL_LAUNCHED("k_visdump");
+    return VPL_OK;
+}
+
+int32_t vpl_closest_hit_batch(const void* d_scene, const void* d_bvh, const float* d_o, const float* d_dir, int64_t n,
+                              float tmin, float tmax, int32_t* d_tri, float* d_t, void* stream) {
+    if (!d_scene || !d_bvh || !d_o || !d_dir || !d_tri || !d_t || n < 0) return VPL_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    SceneHdr hh;
+    VPL_TRY(read_scene_hdr(d_scene, s, &hh));
+    if (n == 0) return VPL_OK;
+    k_closest_batch<<<nb(n, 128), 128, 0, s>>>(bvh_view(d_bvh, hh.n), d_o, d_dir, n, tmin, tmax, d_tri, d_t);
+    VPL_LAUNCHED("k_closest_batch");
+    return VPL_OK;
+}
+
+int32_t vpl_occluded_batch(const void* d_scene, const void* d_bvh, const float* d_a, const float* d_b, int64_t n,
+                           uint8_t* d_occ, void* stream) {
+    if (!d_scene || !d_bvh || !d_a || !d_b || !d_occ || n < 0) return VPL_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    SceneHdr hh;
+    VPL_TRY(read_scene_hdr(d_scene, s, &hh));
+    if (n == 0) return VPL_OK;
+    k_occluded_batch<<<nb(n, 128), 128, 0, s>>>(scene_view(d_scene, hh.n), bvh_view(d_bvh, hh.n), d_a, d_b, n, d_occ);
+    VPL_LAUNCHED("k_occluded_batch");
+    return VPL_OK;
+}
+
+int32_t vpl_philox_batch(const uint32_t* d_in, int64_t n, uint32_t* d_out, void* stream) {
+    if (!d_in || !d_out || n < 0) return VPL_EINVAL;
+    if (n == 0) return VPL_OK;
+    k_philox_batch<<<nb(n, 128), 128, 0, (cudaStream_t)stream>>>(d_in, n, d_out);
+    VPL_LAUNCHED("k_philox_batch");
+    return VPL_OK;
+}
+
+}  // extern "C"
