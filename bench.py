@@ -167,7 +167,7 @@ def run_ours(args):
 
     # pairs per step: front-hit pixels of the whole frame x VPLs
     def hit_pixels():
-        g = r.gbuf.view(-1, 12).view(torch.int32)
+        g = r.gbuf.view(torch.int32).view(-1, 12)
         mine = ((g[:, 3] >= 0) & (g[:, 7] != 0)).sum()
         if world > 1:
             dist.all_reduce(mine)

@@ -199,17 +199,25 @@ def _config1(seed=1):
 
 def _config2(seed=2):
     rng = np.random.default_rng(seed)
+    eye, tgt = np.array([0.25, 1.1, 0.2]), np.array([1.3, 0.75, 1.5])
+    seg = 0.7 * (tgt - eye)
     tris = [room_tris([0, 0, 0], [2, 2, 2], open_front=True)]
     alb = [rng.uniform(0.2, 0.8, (10, 3))]
-    for _ in range(200):
+    placed = 0
+    while placed < 200:
         e = rng.uniform(0.05, 0.4, 3)
         yaw = rng.uniform(0.0, 2 * math.pi)
         c = rng.uniform([0.2, 0.2, 0.2], [1.8, 1.4, 1.8])      # keep the ceiling light clear
+        col = rng.uniform(0.1, 0.9, (1, 3))
+        tt = np.clip((c - eye) @ seg / (seg @ seg), 0.0, 1.0)
+        if np.linalg.norm(c - (eye + tt * seg)) <= 0.5 * np.linalg.norm(e) + 0.1:
+            continue                                           # keep the camera's line of sight clear
         tris.append(box_tris(c, e / 2, yaw))
-        alb.append(np.repeat(rng.uniform(0.1, 0.9, (1, 3)), 12, axis=0))
+        alb.append(np.repeat(col, 12, axis=0))
+        placed += 1
     V = np.concatenate(tris)
     lights = np.stack([make_light([1.0, 2.0 - 1e-3, 1.0])])
-    cam = make_camera([0.25, 1.1, 0.2], [1.3, 0.75, 1.5], 45.0, 512, 512)
+    cam = make_camera(eye, tgt, 45.0, 512, 512)
     M = 4096
     return dict(name="C2", verts=V, albedo=np.concatenate(alb), lights=lights, cam=cam,
                 width=512, height=512, M=M, K_near=_k_near(M, 0.75), max_depth=3, rr=1,
