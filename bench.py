@@ -99,7 +99,7 @@ OPS_PAIR, OPS_TRACED, OPS_BOX, OPS_TRI = 14, 20, 17, 35
 
 
 def algorithmic_ops(ctr):
-    pairs, traced, visible, boxes, tris = (int(x) for x in ctr)
+    pairs, traced, visible, boxes, tris = (int(x) for x in ctr[:5])
     return pairs * OPS_PAIR + traced * OPS_TRACED + boxes * OPS_BOX + tris * OPS_TRI
 
 
@@ -249,7 +249,7 @@ def run_ours(args):
         peak_ops = sm_count * 128 * f_max                      # 4 SMSP x 32 lanes issue per clock
         ops = algorithmic_ops(ctr) / max(world, 1)              # per launch (one rank's share)
         achieved = ops / (t_gather * 1e-3)
-        pairs, traced, visible, boxes, tris = (int(x) for x in ctr)
+        pairs, traced, visible, boxes, tris, wrays, wsteps = (int(x) for x in ctr)
         out = {
             "metric": METRIC, "value": pairs_per_step / (t_step * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
@@ -264,7 +264,9 @@ def run_ours(args):
             "traced_pairs_per_s": traced / (t_gather * 1e-3),
             "counters": {"pairs": pairs, "traced": traced, "visible": visible, "box_tests": boxes,
                          "tri_tests": tris, "box_tests_per_traced": boxes / max(traced, 1),
-                         "tri_tests_per_traced": tris / max(traced, 1)},
+                         "tri_tests_per_traced": tris / max(traced, 1), "warp_rays": wrays,
+                         "warp_steps": wsteps, "lanes_per_warp_ray": traced / max(wrays, 1),
+                         "steps_per_warp_ray": wsteps / max(wrays, 1)},
             "roofline": {"bound": "alu", "kernel": "k_gather", "achieved": achieved / 1e12,
                          "peak": peak_ops / 1e12, "unit": "Tops/s", "frac": achieved / peak_ops,
                          "traffic": None,

@@ -120,6 +120,8 @@ typedef struct {
     unsigned long long visible;    /* traced pairs found unoccluded */
     unsigned long long box_tests;  /* child-box slab tests */
     unsigned long long tri_tests;  /* Moller-Trumbore tests */
+    unsigned long long warp_rays;  /* warp-level shadow-ray packets (>= 1 traced lane) */
+    unsigned long long warp_steps; /* warp-level traversal iterations (node or leaf visits) */
 } vpl_counters;
 
 /* -------------------------------------------------------------------- */

@@ -1,0 +1,397 @@
+// bvh.cu — a2 build_bvh: PLOC (parallel locally-ordered clustering, Meister &
+// Bittner 2018) over Morton-sorted triangles, then a bottom-up SAH pass that
+// collapses small subtrees into leaves of <= 4 triangles, a depth-first
+// triangle ordering so every leaf is a contiguous range, and emission of
+// 64-byte binary nodes (two child boxes + two child refs).  The paper has no
+// acceleration structure; this one only has to make the exact MT visibility
+// and closest-hit queries (DESIGN.md §3 O9) fast.  Boxes are padded by
+// SceneHdr::box_pad so the slab test is conservative w.r.t. the exact MT test.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+
+namespace vplgi {
+
+constexpr int kPlocRadius = 16;
+constexpr int kPlocBlock = 256;
+constexpr int kMaxLeaf = 4;
+constexpr float kCostTri = 1.0f;   // one exact MT test  (~35 thread-ops)
+constexpr float kCostNode = 1.0f;  // one node visit = two slab tests (~34 thread-ops)
+
+__device__ __forceinline__ uint64_t spread21(uint32_t x) {
+    uint64_t v = x & 0x1FFFFFu;
+    v = (v | (v << 32)) & 0x1F00000000FFFFull;
+    v = (v | (v << 16)) & 0x1F0000FF0000FFull;
+    v = (v | (v << 8)) & 0x100F00F00F00F00Full;
+    v = (v | (v << 4)) & 0x10C30C30C30C30C3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+}
+
+__global__ void k_morton63(const SceneHdr* __restrict__ h, const float4* __restrict__ cen, int64_t n,
+                           uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 c = cen[i];
+    float q[3] = {c.x, c.y, c.z};
+    uint32_t qi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float ext = h->bbox_hi[a] - h->bbox_lo[a];
+        float s = ext > 0.0f ? 2097152.0f / ext : 0.0f;
+        float f = fmaxf((q[a] - h->bbox_lo[a]) * s, 0.0f);
+        qi[a] = min((uint32_t)f, 2097151u);
+    }
+    keys[i] = spread21(qi[0]) | (spread21(qi[1]) << 1) | (spread21(qi[2]) << 2);
+    idx[i] = (uint32_t)i;
+}
+
+// cluster = (lo.xyz | ref bits, hi.xyz | 0); ref >= 0 internal node, ~p leaf at Morton position p
+__global__ void k_leaf_clusters(const SceneHdr* __restrict__ h, const float* __restrict__ verts,
+                                const uint32_t* __restrict__ sidx, int64_t n, float4* __restrict__ cl,
+                                float4* __restrict__ lbox) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    float pad = h->box_pad;
+    const float* v = verts + 9 * (int64_t)sidx[p];
+    float lo[3], hi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = fminf(fminf(v[a], v[3 + a]), v[6 + a]) - pad;
+        hi[a] = fmaxf(fmaxf(v[a], v[3 + a]), v[6 + a]) + pad;
+    }
+    float4 L = make_float4(lo[0], lo[1], lo[2], __int_as_float(~(int)p));
+    float4 H = make_float4(hi[0], hi[1], hi[2], 0.0f);
+    cl[2 * p] = L; cl[2 * p + 1] = H;
+    lbox[2 * p] = L; lbox[2 * p + 1] = H;
+}
+
+__device__ __forceinline__ float half_area(float4 lo, float4 hi) {
+    float dx = hi.x - lo.x, dy = hi.y - lo.y, dz = hi.z - lo.z;
+    return dx * dy + dy * dz + dz * dx;
+}
+__device__ __forceinline__ float merged_area(float4 alo, float4 ahi, float4 blo, float4 bhi) {
+    float dx = fmaxf(ahi.x, bhi.x) - fminf(alo.x, blo.x);
+    float dy = fmaxf(ahi.y, bhi.y) - fminf(alo.y, blo.y);
+    float dz = fmaxf(ahi.z, bhi.z) - fminf(alo.z, blo.z);
+    return dx * dy + dy * dz + dz * dx;
+}
+
+// nearest neighbour within +-r in Morton order by merged surface area (ties -> lower index)
+__global__ void __launch_bounds__(kPlocBlock) k_ploc_nn(const float4* __restrict__ cl, int C, int* __restrict__ nn) {
+    __shared__ float4 slo[kPlocBlock + 2 * kPlocRadius], shi[kPlocBlock + 2 * kPlocRadius];
+    int b0 = blockIdx.x * kPlocBlock;
+    for (int k = threadIdx.x; k < kPlocBlock + 2 * kPlocRadius; k += blockDim.x) {
+        int j = b0 - kPlocRadius + k;
+        if (j >= 0 && j < C) { slo[k] = cl[2 * j]; shi[k] = cl[2 * j + 1]; }
+    }
+    __syncthreads();
+    int i = b0 + threadIdx.x;
+    if (i >= C) return;
+    int li = threadIdx.x + kPlocRadius;
+    float4 alo = slo[li], ahi = shi[li];
+    float best = __int_as_float(0x7f800000);
+    int bj = -1;
+    int j0 = max(0, i - kPlocRadius), j1 = min(C - 1, i + kPlocRadius);
+    for (int j = j0; j <= j1; ++j) {
+        if (j == i) continue;
+        int lj = j - b0 + kPlocRadius;
+        float d = merged_area(alo, ahi, slo[lj], shi[lj]);
+        if (d < best) { best = d; bj = j; }   // ascending j: ties keep the lower index
+    }
+    nn[i] = bj;
+}
+
+// flags: bit 32.. = merge (this cluster absorbs nn[i]), bit 0 = keep
+__global__ void k_ploc_flags(const int* __restrict__ nn, int C, unsigned long long* __restrict__ flags) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= C) return;
+    int j = nn[i];
+    bool mutual = j >= 0 && nn[j] == i;
+    unsigned long long merge = (mutual && i < j) ? 1ull : 0ull;
+    unsigned long long keep = (mutual && i > j) ? 0ull : 1ull;
+    flags[i] = (merge << 32) | keep;
+}
+
+__global__ void k_ploc_merge(const float4* __restrict__ cl, const int* __restrict__ nn, int C,
+                             const unsigned long long* __restrict__ flags, const unsigned long long* __restrict__ off,
+                             int next_id, float4* __restrict__ out, int2* __restrict__ child, float4* __restrict__ nbox,
+                             int* __restrict__ parent_int, int* __restrict__ parent_leaf, int* __restrict__ totals) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= C) return;
+    unsigned long long f = flags[i], o = off[i];
+    int keep = (int)(f & 1ull), merge = (int)(f >> 32);
+    int ko = (int)(o & 0xFFFFFFFFull), mo = (int)(o >> 32);
+    if (i == C - 1) { totals[0] = ko + keep; totals[1] = mo + merge; }
+    if (!keep) return;
+    float4 alo = cl[2 * i], ahi = cl[2 * i + 1];
+    if (!merge) {
+        out[2 * ko] = alo; out[2 * ko + 1] = ahi;
+        return;
+    }
+    int j = nn[i];
+    float4 blo = cl[2 * j], bhi = cl[2 * j + 1];
+    int id = next_id - mo;
+    int ra = __float_as_int(alo.w), rb = __float_as_int(blo.w);
+    child[id] = make_int2(ra, rb);
+    if (ra >= 0) parent_int[ra] = id; else parent_leaf[~ra] = id;
+    if (rb >= 0) parent_int[rb] = id; else parent_leaf[~rb] = id;
+    float4 L = make_float4(fminf(alo.x, blo.x), fminf(alo.y, blo.y), fminf(alo.z, blo.z), __int_as_float(id));
+    float4 H = make_float4(fmaxf(ahi.x, bhi.x), fmaxf(ahi.y, bhi.y), fmaxf(ahi.z, bhi.z), 0.0f);
+    nbox[2 * id] = L; nbox[2 * id + 1] = H;
+    out[2 * ko] = L; out[2 * ko + 1] = H;
+}
+
+// bottom-up: triangle counts and SAH cost; collapse subtrees of <= kMaxLeaf triangles when cheaper
+__global__ void k_sah_collapse(int64_t n, const int2* __restrict__ child, const float4* __restrict__ nbox,
+                               const float4* __restrict__ lbox, const int* __restrict__ parent_int,
+                               const int* __restrict__ parent_leaf, int* __restrict__ flags, int* __restrict__ cnt,
+                               float* __restrict__ cost, uint8_t* __restrict__ collapsed) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int node = parent_leaf[p];
+    while (node >= 0) {
+        __threadfence();
+        if (atomicAdd(&flags[node], 1) == 0) return;
+        __threadfence();
+        int2 c = child[node];
+        int cn[2];
+        float cc[2], ca[2];
+        int refs[2] = {c.x, c.y};
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            int r = refs[k];
+            if (r >= 0) {
+                cn[k] = __ldcg(cnt + r);
+                cc[k] = __ldcg(cost + r);
+                ca[k] = half_area(nbox[2 * r], nbox[2 * r + 1]);
+            } else {
+                cn[k] = 1;
+                cc[k] = kCostTri;
+                ca[k] = half_area(lbox[2 * (~r)], lbox[2 * (~r) + 1]);
+            }
+        }
+        int total = cn[0] + cn[1];
+        float an = half_area(nbox[2 * node], nbox[2 * node + 1]);
+        float c_int = kCostNode + (an > 0.0f ? (ca[0] * cc[0] + ca[1] * cc[1]) / an : cc[0] + cc[1]);
+        float c_leaf = kCostTri * (float)total;
+        bool col = total <= kMaxLeaf && c_leaf <= c_int && node != 0;
+        __stcg(cnt + node, total);
+        __stcg(cost + node, col ? c_leaf : c_int);
+        collapsed[node] = col;
+        node = parent_int[node];
+    }
+}
+
+// depth-first triangle offset of every node (leaves: index ~p -> slot n-1+p)
+__global__ void k_dfs_offsets(int64_t n, const int2* __restrict__ child, const int* __restrict__ parent_int,
+                              const int* __restrict__ parent_leaf, const int* __restrict__ cnt, int* __restrict__ off,
+                              int* __restrict__ max_depth) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= 2 * n - 1) return;
+    int self = k < n - 1 ? (int)k : ~(int)(k - (n - 1));
+    int node = self;
+    int par = node >= 0 ? parent_int[node] : parent_leaf[~node];
+    int o = 0, depth = 0;
+    while (par >= 0) {
+        int2 c = child[par];
+        if (c.y == node) o += c.x >= 0 ? cnt[c.x] : 1;
+        node = par;
+        par = parent_int[node];
+        ++depth;
+    }
+    off[k] = o;
+    if (self < 0) atomicMax(max_depth, depth);
+}
+
+__device__ __forceinline__ int leaf_ref(int first, int count) { return ~((first << 3) | (count - 1)); }
+
+__global__ void k_emit_nodes(int64_t n, const int2* __restrict__ child, const float4* __restrict__ nbox,
+                             const float4* __restrict__ lbox, const int* __restrict__ cnt, const int* __restrict__ off,
+                             const uint8_t* __restrict__ collapsed, float4* __restrict__ nodes) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n - 1 || collapsed[i]) return;
+    int2 c = child[i];
+    int refs[2] = {c.x, c.y};
+    float4 lo[2], hi[2];
+    int out[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        int r = refs[k];
+        if (r >= 0) {
+            lo[k] = nbox[2 * r]; hi[k] = nbox[2 * r + 1];
+            out[k] = collapsed[r] ? leaf_ref(off[r], cnt[r]) : r;
+        } else {
+            lo[k] = lbox[2 * (~r)]; hi[k] = lbox[2 * (~r) + 1];
+            out[k] = leaf_ref(off[(n - 1) + (~r)], 1);
+        }
+    }
+    // order children along the axis of largest centre separation (child 0 = lower centre) and
+    // store that axis in n3.z: packet traversal visits child 0 first iff the packet travels +axis
+    float dc[3] = {(lo[1].x + hi[1].x) - (lo[0].x + hi[0].x), (lo[1].y + hi[1].y) - (lo[0].y + hi[0].y),
+                   (lo[1].z + hi[1].z) - (lo[0].z + hi[0].z)};
+    int axis = 0;
+    if (fabsf(dc[1]) > fabsf(dc[axis])) axis = 1;
+    if (fabsf(dc[2]) > fabsf(dc[axis])) axis = 2;
+    if (dc[axis] < 0.0f) {
+        float4 tl = lo[0], th = hi[0];
+        lo[0] = lo[1]; hi[0] = hi[1]; lo[1] = tl; hi[1] = th;
+        int to = out[0]; out[0] = out[1]; out[1] = to;
+    }
+    nodes[4 * i + 0] = make_float4(lo[0].x, hi[0].x, lo[0].y, hi[0].y);
+    nodes[4 * i + 1] = make_float4(lo[1].x, hi[1].x, lo[1].y, hi[1].y);
+    nodes[4 * i + 2] = make_float4(lo[0].z, hi[0].z, lo[1].z, hi[1].z);
+    nodes[4 * i + 3] = make_float4(__int_as_float(out[0]), __int_as_float(out[1]), __int_as_float(axis), 0.0f);
+}
+
+__global__ void k_emit_tris(const float* __restrict__ verts, const uint32_t* __restrict__ sidx, int64_t n,
+                            const int* __restrict__ off, float4* __restrict__ tris) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    uint32_t t = sidx[p];
+    int slot = n > 1 ? off[(n - 1) + p] : 0;
+    const float* v = verts + 9 * (int64_t)t;
+    f3 v0 = ld3(v), e1 = ld3(v + 3) - v0, e2 = ld3(v + 6) - v0;
+    tris[3 * slot + 0] = make_float4(v0.x, v0.y, v0.z, __int_as_float((int)t));
+    tris[3 * slot + 1] = make_float4(e1.x, e1.y, e1.z, 0.0f);
+    tris[3 * slot + 2] = make_float4(e2.x, e2.y, e2.z, 0.0f);
+}
+
+struct BuildWork {
+    uint64_t *keys, *keys2;
+    uint32_t *idx, *idx2;
+    float4 *clA, *clB, *lbox, *nbox;
+    int *nn, *parent_int, *parent_leaf, *flags, *cnt, *off, *totals;
+    unsigned long long *mflags, *moff;
+    float* cost;
+    uint8_t* collapsed;
+    int2* child;
+    void* cub;
+    size_t cub_bytes;
+};
+
+static size_t build_layout(int64_t n, char* base, BuildWork* w) {
+    Bump b{base};
+    w->keys = b.take<uint64_t>(n);
+    w->keys2 = b.take<uint64_t>(n);
+    w->idx = b.take<uint32_t>(n);
+    w->idx2 = b.take<uint32_t>(n);
+    w->clA = b.take<float4>(2 * n);
+    w->clB = b.take<float4>(2 * n);
+    w->lbox = b.take<float4>(2 * n);
+    w->nbox = b.take<float4>(2 * n);
+    w->nn = b.take<int>(n);
+    w->parent_int = b.take<int>(n);
+    w->parent_leaf = b.take<int>(n);
+    w->flags = b.take<int>(n);
+    w->cnt = b.take<int>(n);
+    w->off = b.take<int>(2 * n);
+    w->totals = b.take<int>(4);
+    w->mflags = b.take<unsigned long long>(n);
+    w->moff = b.take<unsigned long long>(n);
+    w->cost = b.take<float>(n);
+    w->collapsed = b.take<uint8_t>(n);
+    w->child = b.take<int2>(n);
+    size_t c1 = 0, c2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, c1, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
+                                    (uint32_t*)nullptr, (int)n, 0, 64);
+    cub::DeviceScan::ExclusiveSum(nullptr, c2, (unsigned long long*)nullptr, (unsigned long long*)nullptr, (int)n);
+    w->cub_bytes = c1 > c2 ? c1 : c2;
+    w->cub = b.take<char>(w->cub_bytes);
+    return b.off;
+}
+
+static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+}  // namespace vplgi
+
+using namespace vplgi;
+
+extern "C" {
+
+int32_t vpl_bvh_bytes(int64_t n_tris, size_t* bvh_bytes, size_t* work_bytes) {
+    if (!bvh_bytes || !work_bytes || n_tris <= 0 || n_tris > (int64_t)1 << 28) return VPL_EINVAL;
+    *bvh_bytes = bvh_layout(n_tris, nullptr);
+    BuildWork w;
+    *work_bytes = build_layout(n_tris, nullptr, &w);
+    return VPL_OK;
+}
+
+int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* d_work, size_t work_bytes,
+                      void* stream) {
+    if (!d_scene || !d_bvh || !d_work) { set_error("vpl_build_bvh: null pointer"); return VPL_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    SceneHdr hh;
+    VPL_TRY(read_scene_hdr(d_scene, s, &hh));
+    const int64_t n = hh.n;
+    size_t nb = 0, wb = 0;
+    VPL_TRY(vpl_bvh_bytes(n, &nb, &wb));
+    if (bvh_bytes < nb || work_bytes < wb) { set_error("vpl_build_bvh: buffers too small"); return VPL_ESMALL; }
+    SceneView sv = scene_view(d_scene, n);
+    BvhHdr bh;
+    bvh_layout(n, &bh);
+    VPL_CUDA(cudaMemcpyAsync(d_bvh, &bh, sizeof(bh), cudaMemcpyHostToDevice, s));
+    float4* nodes = (float4*)((char*)d_bvh + bh.off_nodes);
+    float4* tris = (float4*)((char*)d_bvh + bh.off_tris);
+    BuildWork w;
+    build_layout(n, (char*)d_work, &w);
+
+    // Morton order of centroids over the scene box
+    k_morton63<<<nblk(n, 256), 256, 0, s>>>(sv.hdr, sv.cen, n, w.keys, w.idx);
+    VPL_LAUNCHED("k_morton63");
+    size_t cb = w.cub_bytes;
+    VPL_CUDA(cub::DeviceRadixSort::SortPairs(w.cub, cb, w.keys, w.keys2, w.idx, w.idx2, (int)n, 0, 64, s));
+    k_leaf_clusters<<<nblk(n, 256), 256, 0, s>>>(sv.hdr, sv.verts, w.idx2, n, w.clA, w.lbox);
+    VPL_LAUNCHED("k_leaf_clusters");
+
+    if (n > 1) {
+        // PLOC: merge mutual nearest neighbours until one cluster is left
+        int C = (int)n, next_id = (int)n - 2;
+        float4 *cur = w.clA, *nxt = w.clB;
+        VPL_CUDA(cudaMemsetAsync(w.parent_int, 0xFF, sizeof(int) * n, s));
+        int tot[2];
+        while (C > 1) {
+            k_ploc_nn<<<nblk(C, kPlocBlock), kPlocBlock, 0, s>>>(cur, C, w.nn);
+            VPL_LAUNCHED("k_ploc_nn");
+            k_ploc_flags<<<nblk(C, 256), 256, 0, s>>>(w.nn, C, w.mflags);
+            VPL_LAUNCHED("k_ploc_flags");
+            cb = w.cub_bytes;
+            VPL_CUDA(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.mflags, w.moff, C, s));
+            k_ploc_merge<<<nblk(C, 256), 256, 0, s>>>(cur, w.nn, C, w.mflags, w.moff, next_id, nxt, w.child, w.nbox,
+                                                      w.parent_int, w.parent_leaf, w.totals);
+            VPL_LAUNCHED("k_ploc_merge");
+            VPL_CUDA(cudaMemcpyAsync(tot, w.totals, sizeof(tot), cudaMemcpyDeviceToHost, s));
+            VPL_CUDA(cudaStreamSynchronize(s));
+            if (tot[1] <= 0) { set_error("vpl_build_bvh: PLOC made no progress"); return VPL_ECUDA; }
+            C = tot[0];
+            next_id -= tot[1];
+            float4* t = cur; cur = nxt; nxt = t;
+        }
+        // SAH collapse, depth-first ordering, emission
+        VPL_CUDA(cudaMemsetAsync(w.flags, 0, sizeof(int) * n, s));
+        k_sah_collapse<<<nblk(n, 256), 256, 0, s>>>(n, w.child, w.nbox, w.lbox, w.parent_int, w.parent_leaf, w.flags,
+                                                    w.cnt, w.cost, w.collapsed);
+        VPL_LAUNCHED("k_sah_collapse");
+        VPL_CUDA(cudaMemsetAsync(w.totals + 2, 0, sizeof(int), s));
+        k_dfs_offsets<<<nblk(2 * n - 1, 256), 256, 0, s>>>(n, w.child, w.parent_int, w.parent_leaf, w.cnt, w.off,
+                                                           w.totals + 2);
+        VPL_LAUNCHED("k_dfs_offsets");
+        k_emit_nodes<<<nblk(n - 1, 256), 256, 0, s>>>(n, w.child, w.nbox, w.lbox, w.cnt, w.off, w.collapsed, nodes);
+        VPL_LAUNCHED("k_emit_nodes");
+    }
+    k_emit_tris<<<nblk(n, 256), 256, 0, s>>>(sv.verts, w.idx2, n, w.off, tris);
+    VPL_LAUNCHED("k_emit_tris");
+    if (n > 1) {
+        int depth = 0;
+        VPL_CUDA(cudaMemcpyAsync(&depth, w.totals + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
+        VPL_CUDA(cudaStreamSynchronize(s));
+        if (depth >= kStack) {
+            set_error("vpl_build_bvh: tree depth %d exceeds the traversal stack (%d)", depth, kStack);
+            return VPL_ECUDA;
+        }
+    }
+    return VPL_OK;
+}
+
+}  // extern "C"

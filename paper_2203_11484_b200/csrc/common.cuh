@@ -228,11 +228,19 @@ __device__ __forceinline__ bool mt_hit(f3 o, f3 d, float4 a, float4 b, float4 c,
 
 struct TravStats {
     uint32_t boxes = 0, tris = 0;
+    uint32_t wrays = 0, wsteps = 0;  // warp-level packets / iterations (counted on lane 0)
 };
 
-constexpr int kStack = 96;
+// leaf refs: ~((first << 3) | (count - 1)), count in [1, 8]
+__device__ __forceinline__ void leaf_range(int node, int& first, int& count) {
+    int p = ~node;
+    first = p >> 3;
+    count = (p & 7) + 1;
+}
 
-// Any hit in (tmin, tmax): true if some triangle's MT hit lies inside.
+constexpr int kStack = 128;  // > max tree depth, checked at build time (vpl_build_bvh)
+
+// Any hit in (tmin, tmax), one ray per thread.
 template <bool kCount>
 __device__ __forceinline__ bool bvh_any_hit(const BvhView& bv, const Ray& r, TravStats* st) {
     int stack[kStack];
@@ -249,18 +257,21 @@ __device__ __forceinline__ bool bvh_any_hit(const BvhView& bv, const Ray& r, Tra
             int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
             if (h0 && h1) {
                 bool first0 = t0 <= t1;
-                if (sp < kStack) stack[sp++] = first0 ? c1 : c0;
+                stack[sp++] = first0 ? c1 : c0;
                 node = first0 ? c0 : c1;
                 continue;
             }
             if (h0) { node = c0; continue; }
             if (h1) { node = c1; continue; }
         } else {
-            int p = ~node;
-            const float4* tr = bv.tris + 3 * p;
-            float t;
-            if (kCount) st->tris += 1;
-            if (mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t)) return true;
+            int first, count;
+            leaf_range(node, first, count);
+            for (int k = 0; k < count; ++k) {
+                const float4* tr = bv.tris + 3 * (first + k);
+                float t;
+                if (kCount) st->tris += 1;
+                if (mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t)) return true;
+            }
         }
         if (sp == 0) return false;
         node = stack[--sp];
@@ -274,7 +285,6 @@ __device__ __forceinline__ int bvh_closest(const BvhView& bv, const Ray& r, floa
     int node = bv.root;
     int best = -1;
     float tb = r.tmax;
-    t_best = r.tmax;
     while (true) {
         if (node >= 0) {
             const float4* nd = bv.nodes + 4 * node;
@@ -286,21 +296,24 @@ __device__ __forceinline__ int bvh_closest(const BvhView& bv, const Ray& r, floa
             int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
             if (h0 && h1) {
                 bool first0 = t0 <= t1;
-                if (sp < kStack) stack[sp++] = first0 ? c1 : c0;
+                stack[sp++] = first0 ? c1 : c0;
                 node = first0 ? c0 : c1;
                 continue;
             }
             if (h0) { node = c0; continue; }
             if (h1) { node = c1; continue; }
         } else {
-            int p = ~node;
-            const float4* tr = bv.tris + 3 * p;
-            float4 a = __ldg(tr);
-            float t;
-            // hit test against the ORIGINAL (tmin, tmax); order against the best so far
-            if (mt_hit(r.o, r.d, a, __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t)) {
-                int orig = __float_as_int(a.w);
-                if (t < tb || (t == tb && orig < best)) { tb = t; best = orig; }
+            int first, count;
+            leaf_range(node, first, count);
+            for (int k = 0; k < count; ++k) {
+                const float4* tr = bv.tris + 3 * (first + k);
+                float4 a = __ldg(tr);
+                float t;
+                // hit test against the ORIGINAL (tmin, tmax); order against the best so far
+                if (mt_hit(r.o, r.d, a, __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t)) {
+                    int orig = __float_as_int(a.w);
+                    if (t < tb || (t == tb && orig < best)) { tb = t; best = orig; }
+                }
             }
         }
         if (sp == 0) break;
@@ -310,16 +323,93 @@ __device__ __forceinline__ int bvh_closest(const BvhView& bv, const Ray& r, floa
     return best;
 }
 
-// unoccluded(a, b) with the eps-shrunk segment (O9)
-template <bool kCount>
-__device__ __forceinline__ bool segment_occluded(const BvhView& bv, f3 a, f3 b, float eps, TravStats* st) {
+// unoccluded(a, b) with the eps-shrunk segment (O9) — segment setup shared by
+// the per-thread and the warp-cooperative traversals
+__device__ __forceinline__ bool segment_ray(f3 a, f3 b, float eps, Ray& r) {
     f3 d = b - a;
     float dist = sqrtf(dot(d, d));
     f3 dir = mk3(d.x / dist, d.y / dist, d.z / dist);
     float tmin = eps, tmax = dist - eps;
     if (!(tmax > tmin)) return false;
-    Ray r = make_ray(a, dir, tmin, tmax);
+    r = make_ray(a, dir, tmin, tmax);
+    return true;
+}
+
+template <bool kCount>
+__device__ __forceinline__ bool segment_occluded(const BvhView& bv, f3 a, f3 b, float eps, TravStats* st) {
+    Ray r;
+    if (!segment_ray(a, b, eps, r)) return false;
     return bvh_any_hit<kCount>(bv, r, st);
+}
+
+// Warp-cooperative any-hit (packet traversal): the 32 lanes carry their own
+// rays but walk ONE node sequence — a child is entered if any live lane's ray
+// enters its box — so node and triangle fetches are warp-uniform broadcasts
+// and the traversal stack is warp-uniform (shared memory, one slot per level).
+// A lane may test triangles its own boxes would have culled; that cannot
+// change an any-hit result, so each lane's answer equals bvh_any_hit's.
+// Children are visited in the order of the node's split axis and the packet
+// leader's direction sign (dir_neg bit a = leader's dir[a] < 0).
+// `cache` (in/out, per lane): leaf-order index of the last occluder found; it
+// is tested first (exact MT), which resolves coherent occluded rays without a
+// traversal.  Must be called by all 32 lanes with the same sstack.
+template <bool kCount>
+__device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, bool live, int& cache,
+                                             int* __restrict__ sstack, TravStats* st) {
+    bool occl = false;
+    if (live && cache >= 0) {
+        const float4* tr = bv.tris + 3 * cache;
+        float t;
+        if (kCount) st->tris += 1;
+        occl = mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t);
+    }
+    unsigned need = __ballot_sync(0xFFFFFFFFu, live && !occl);
+    if (!need) return occl;
+    int leader = __ffs(need) - 1;
+    unsigned neg = (r.d.x < 0.0f ? 1u : 0u) | (r.d.y < 0.0f ? 2u : 0u) | (r.d.z < 0.0f ? 4u : 0u);
+    const unsigned dir_neg = __shfl_sync(0xFFFFFFFFu, neg, leader);
+    if (kCount && (threadIdx.x & 31) == 0) st->wrays += 1;
+    int sp = 0;
+    int node = bv.root;
+    while (true) {
+        const bool go = live && !occl;
+        if (kCount && (threadIdx.x & 31) == 0) st->wsteps += 1;
+        if (node >= 0) {
+            const float4* nd = bv.nodes + 4 * node;
+            float4 n0 = __ldg(nd + 0), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
+            float t0, t1;
+            bool h0 = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, r.tmax, t0) & go;
+            bool h1 = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, r.tmax, t1) & go;
+            if (kCount && go) st->boxes += 2;
+            unsigned b0 = __ballot_sync(0xFFFFFFFFu, h0), b1 = __ballot_sync(0xFFFFFFFFu, h1);
+            int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
+            if (b0 | b1) {
+                if (b0 && b1) {
+                    bool rev = (dir_neg >> __float_as_int(n3.z)) & 1u;
+                    sstack[sp++] = rev ? c0 : c1;
+                    node = rev ? c1 : c0;
+                } else {
+                    node = b0 ? c0 : c1;
+                }
+                continue;
+            }
+        } else {
+            int first, count;
+            leaf_range(node, first, count);
+            for (int k = 0; k < count; ++k) {
+                const float4* tr = bv.tris + 3 * (first + k);
+                float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
+                float t;
+                bool hit = mt_hit(r.o, r.d, a, b, c, r.tmin, r.tmax, t) & go & !occl;
+                if (kCount && go && !occl) st->tris += 1;
+                if (hit) { occl = true; cache = first + k; }
+            }
+            if (!__any_sync(0xFFFFFFFFu, live && !occl)) break;
+        }
+        if (sp == 0) break;
+        node = sstack[--sp];
+    }
+    return occl;
 }
 
 // tile -> pixel mapping: warp w of a call covers an 8x4 block

@@ -65,7 +65,9 @@ template <bool kCount>
 __global__ void __launch_bounds__(128) k_gather(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb,
                                                 const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
                                                 vpl_counters* __restrict__ ctr, int* __restrict__ queue) {
+    __shared__ int s_stack[4][kStack];
     const int lane = threadIdx.x & 31;
+    int* sstack = s_stack[threadIdx.x >> 5];
     const int64_t nw = tm.n_warps();
     const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
     while (true) {
@@ -85,6 +87,7 @@ __global__ void __launch_bounds__(128) k_gather(SceneView sv, BvhView bv, TileMa
             x = xyz(a); nx = xyz(b); rho = xyz(c);
         }
         float acc[3] = {0.0f, 0.0f, 0.0f};
+        int cache = -1;
         TravStats st;
         unsigned long long n_traced = 0, n_vis = 0;
         if (__any_sync(0xFFFFFFFFu, active)) {
@@ -93,14 +96,17 @@ __global__ void __launch_bounds__(128) k_gather(SceneView sv, BvhView bv, TileMa
                 int i1 = min(M, i0 + 256);
                 for (int i = i0; i < i1; ++i) {
                     VplGeo v = load_vpl(vpls + i);
-                    if (!active || v.tri == tri_x) continue;
                     f3 d = v.y - x;
                     float r2 = dot(d, d);
                     float cx = dot(nx, d);
                     float ci = -dot(v.n, d);
-                    if (!(cx > 0.0f && ci > 0.0f)) continue;
-                    if (kCount) ++n_traced;
-                    if (segment_occluded<kCount>(bv, x, v.y, eps, &st)) continue;
+                    bool traced = active && v.tri != tri_x && cx > 0.0f && ci > 0.0f;
+                    if (!__any_sync(0xFFFFFFFFu, traced)) continue;       // warp-uniform skip
+                    Ray ray;
+                    bool live = traced && segment_ray(x, v.y, eps, ray);
+                    bool occl = warp_any_hit<kCount>(bv, ray, live, cache, sstack, &st);
+                    if (kCount && traced) ++n_traced;
+                    if (!traced || occl) continue;
                     if (kCount) ++n_vis;
                     float w = __fdividef(cx * ci, r2 * fmaxf(r2, b2));
                     part[0] = fmaf(v.phi.x, w, part[0]);
@@ -119,7 +125,7 @@ __global__ void __launch_bounds__(128) k_gather(SceneView sv, BvhView bv, TileMa
         }
         if (kCount) {
             unsigned long long pairs = active ? (unsigned long long)M : 0ull;
-            unsigned long long bx = st.boxes, tt = st.tris;
+            unsigned long long bx = st.boxes, tt = st.tris, wr = st.wrays, ws = st.wsteps;
             for (int o = 16; o > 0; o >>= 1) {
                 pairs += __shfl_xor_sync(0xFFFFFFFFu, pairs, o);
                 n_traced += __shfl_xor_sync(0xFFFFFFFFu, n_traced, o);
@@ -133,38 +139,50 @@ __global__ void __launch_bounds__(128) k_gather(SceneView sv, BvhView bv, TileMa
                 atomicAdd(&ctr->visible, n_vis);
                 atomicAdd(&ctr->box_tests, bx);
                 atomicAdd(&ctr->tri_tests, tt);
+                atomicAdd(&ctr->warp_rays, wr);
+                atomicAdd(&ctr->warp_steps, ws);
             }
         }
     }
 }
 
-// test hook: traced / visible bits of listed pixels x all VPLs (same code path)
+// test hook: traced / visible bits of listed pixels x all VPLs, through the
+// gather's own warp-cooperative traversal (lanes = 32 consecutive listed pixels)
 __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict__ gb, const vpl_record* __restrict__ vpls,
                           int32_t M, const int32_t* __restrict__ pixels, int32_t n_px, uint32_t* __restrict__ tbits,
                           uint32_t* __restrict__ vbits) {
+    __shared__ int s_stack[2][kStack];
+    int* sstack = s_stack[threadIdx.x >> 5];
     int64_t words = (M + 31) / 32;
-    int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (id >= (int64_t)n_px * words) return;
-    int32_t k = (int32_t)(id / words), wd = (int32_t)(id % words);
-    const vpl_gpoint* g = gb + pixels[k];
-    uint32_t tb = 0, vb = 0;
-    if (g->tri >= 0 && g->front) {
-        f3 x = ld3(g->pos), nx = ld3(g->nrm);
+    int lane = threadIdx.x & 31;
+    int cache = -1;
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if ((k - lane) >= n_px) return;                      // whole warp out of range
+    bool inb = k < n_px;
+    const vpl_gpoint* g = gb + (inb ? pixels[k] : 0);
+    bool active = inb && g->tri >= 0 && g->front;
+    f3 x = ld3(g->pos), nx = ld3(g->nrm);
+    int tri_x = g->tri;
+    float eps = sv.hdr->eps;
+    for (int64_t wd = 0; wd < words; ++wd) {
+        uint32_t tb = 0, vb = 0;
         for (int b = 0; b < 32; ++b) {
-            int i = wd * 32 + b;
+            int i = (int)(wd * 32 + b);
             if (i >= M) break;
             VplGeo v = load_vpl(vpls + i);
-            if (v.tri == g->tri) continue;
             f3 d = v.y - x;
             float cx = dot(nx, d);
             float ci = -dot(v.n, d);
-            if (!(cx > 0.0f && ci > 0.0f)) continue;
-            tb |= 1u << b;
-            if (!segment_occluded<false>(bv, x, v.y, sv.hdr->eps, nullptr)) vb |= 1u << b;
+            bool traced = active && v.tri != tri_x && cx > 0.0f && ci > 0.0f;
+            if (!__any_sync(0xFFFFFFFFu, traced)) continue;
+            Ray ray;
+            bool live = traced && segment_ray(x, v.y, eps, ray);
+            bool occl = warp_any_hit<false>(bv, ray, live, cache, sstack, nullptr);
+            if (traced) tb |= 1u << b;
+            if (traced && !occl) vb |= 1u << b;
         }
+        if (inb) { tbits[k * words + wd] = tb; vbits[k * words + wd] = vb; }
     }
-    tbits[id] = tb;
-    vbits[id] = vb;
 }
 
 __global__ void k_closest_batch(BvhView bv, const float* __restrict__ o, const float* __restrict__ d, int64_t n,
@@ -277,9 +295,8 @@ int32_t vpl_visibility_dump(const void* d_scene, const void* d_bvh, const vpl_gp
     cudaStream_t s = (cudaStream_t)stream;
     SceneHdr hh;
     VPL_TRY(read_scene_hdr(d_scene, s, &hh));
-    int64_t total = (int64_t)n_pixels * ((n_vpls + 31) / 32);
-    if (total == 0) return VPL_OK;
-    k_visdump<<<nb(total, 64), 64, 0, s>>>(scene_view(d_scene, hh.n), bvh_view(d_bvh, hh.n), d_gbuf, d_vpls, n_vpls,
+    if (n_pixels == 0) return VPL_OK;
+    k_visdump<<<nb(n_pixels, 64), 64, 0, s>>>(scene_view(d_scene, hh.n), bvh_view(d_bvh, hh.n), d_gbuf, d_vpls, n_vpls,
                                            d_pixels, n_pixels, d_traced_bits, d_vis_bits);
     VPL_LAUNCHED("k_visdump");
     return VPL_OK;

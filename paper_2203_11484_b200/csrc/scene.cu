@@ -1,6 +1,4 @@
-// scene.cu — a1 scene_upload (O1), a3 classify_near_far (O2), a2 build_bvh (LBVH).
-#include <cub/device/device_radix_sort.cuh>
-
+// scene.cu — a1 scene_upload (O1) and a3 classify_near_far (O2).
 #include "common.cuh"
 
 namespace vplgi {
@@ -118,171 +116,6 @@ __global__ void k_i64_from_ull(const unsigned long long* a, int64_t* b) {
     if (threadIdx.x == 0 && blockIdx.x == 0) *b = (int64_t)*a;
 }
 
-// ------------------------------------------------------------------ LBVH (Karras 2012)
-__device__ __forceinline__ uint64_t spread21(uint32_t x) {
-    uint64_t v = x & 0x1FFFFFu;
-    v = (v | (v << 32)) & 0x1F00000000FFFFull;
-    v = (v | (v << 16)) & 0x1F0000FF0000FFull;
-    v = (v | (v << 8)) & 0x100F00F00F00F00Full;
-    v = (v | (v << 4)) & 0x10C30C30C30C30C3ull;
-    v = (v | (v << 2)) & 0x1249249249249249ull;
-    return v;
-}
-
-__global__ void k_morton63(const SceneHdr* __restrict__ h, const float4* __restrict__ cen, int64_t n,
-                           uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    f3 c = xyz(cen[i]);
-    const float* lo = h->bbox_lo;
-    const float* hi = h->bbox_hi;
-    float q[3] = {c.x, c.y, c.z};
-    uint32_t qi[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        float ext = hi[a] - lo[a];
-        float s = ext > 0.0f ? 2097152.0f / ext : 0.0f;
-        float f = fmaxf((q[a] - lo[a]) * s, 0.0f);
-        qi[a] = min((uint32_t)f, 2097151u);
-    }
-    keys[i] = spread21(qi[0]) | (spread21(qi[1]) << 1) | (spread21(qi[2]) << 2);
-    idx[i] = (uint32_t)i;
-}
-
-__device__ __forceinline__ int delta(const uint64_t* __restrict__ k, int64_t n, int64_t i, int64_t j) {
-    if (j < 0 || j >= n) return -1;
-    uint64_t a = k[i], b = k[j];
-    if (a == b) return 64 + __clz((uint32_t)(i ^ j));
-    return __clzll(a ^ b);
-}
-
-// child refs: >= 0 internal node, ~p leaf at sorted position p
-__global__ void k_karras(const uint64_t* __restrict__ k, int64_t n, int2* __restrict__ child,
-                         int32_t* __restrict__ parent_int, int32_t* __restrict__ parent_leaf) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n - 1) return;
-    int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
-    int dmin = delta(k, n, i, i - d);
-    int64_t lmax = 2;
-    while (delta(k, n, i, i + lmax * d) > dmin) lmax <<= 1;
-    int64_t l = 0;
-    for (int64_t t = lmax >> 1; t >= 1; t >>= 1)
-        if (delta(k, n, i, i + (l + t) * d) > dmin) l += t;
-    int64_t j = i + l * d;
-    int dnode = delta(k, n, i, j);
-    int64_t s = 0;
-    int64_t t = l;
-    do {
-        t = (t + 1) >> 1;
-        if (delta(k, n, i, i + (s + t) * d) > dnode) s += t;
-    } while (t > 1);
-    int64_t g = i + s * d + min(d, 0);
-    int left = (min(i, j) == g) ? ~(int)g : (int)g;
-    int right = (max(i, j) == g + 1) ? ~(int)(g + 1) : (int)(g + 1);
-    child[i] = make_int2(left, right);
-    if (left >= 0) parent_int[left] = (int)i; else parent_leaf[~left] = (int)i;
-    if (right >= 0) parent_int[right] = (int)i; else parent_leaf[~right] = (int)i;
-    if (i == 0) parent_int[0] = -1;
-}
-
-struct Box { float lo[3], hi[3]; };
-
-__device__ __forceinline__ void store_box(float* dst, const Box& b) {
-    for (int a = 0; a < 3; ++a) { __stcg(dst + a, b.lo[a]); __stcg(dst + 3 + a, b.hi[a]); }
-}
-__device__ __forceinline__ Box load_box(const float* src) {
-    Box b;
-    for (int a = 0; a < 3; ++a) { b.lo[a] = __ldcg(src + a); b.hi[a] = __ldcg(src + 3 + a); }
-    return b;
-}
-
-// bottom-up refit: the second child to arrive computes the union
-__global__ void k_refit(const SceneHdr* __restrict__ h, const float* __restrict__ verts, const uint32_t* __restrict__ sidx,
-                        int64_t n, const int2* __restrict__ child, const int32_t* __restrict__ parent_int,
-                        const int32_t* __restrict__ parent_leaf, int32_t* __restrict__ flags,
-                        float* __restrict__ leafbox, float* __restrict__ intbox) {
-    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    float pad = h->box_pad;
-    const float* v = verts + 9 * (int64_t)sidx[p];
-    Box b;
-    for (int a = 0; a < 3; ++a) {
-        b.lo[a] = fminf(fminf(v[a], v[3 + a]), v[6 + a]) - pad;
-        b.hi[a] = fmaxf(fmaxf(v[a], v[3 + a]), v[6 + a]) + pad;
-    }
-    store_box(leafbox + 6 * p, b);
-    if (n == 1) return;
-    __threadfence();
-    int node = parent_leaf[p];
-    while (node >= 0) {
-        if (atomicAdd(&flags[node], 1) == 0) return;
-        __threadfence();
-        int2 c = child[node];
-        Box a = c.x >= 0 ? load_box(intbox + 6 * c.x) : load_box(leafbox + 6 * (~c.x));
-        Box bb = c.y >= 0 ? load_box(intbox + 6 * c.y) : load_box(leafbox + 6 * (~c.y));
-        Box u;
-        for (int k = 0; k < 3; ++k) { u.lo[k] = fminf(a.lo[k], bb.lo[k]); u.hi[k] = fmaxf(a.hi[k], bb.hi[k]); }
-        store_box(intbox + 6 * node, u);
-        __threadfence();
-        node = parent_int[node];
-    }
-}
-
-__global__ void k_pack_nodes(int64_t n, const int2* __restrict__ child, const float* __restrict__ leafbox,
-                             const float* __restrict__ intbox, float4* __restrict__ nodes) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n - 1) return;
-    int2 c = child[i];
-    const float* a = c.x >= 0 ? intbox + 6 * c.x : leafbox + 6 * (~c.x);
-    const float* b = c.y >= 0 ? intbox + 6 * c.y : leafbox + 6 * (~c.y);
-    nodes[4 * i + 0] = make_float4(a[0], a[3], a[1], a[4]);
-    nodes[4 * i + 1] = make_float4(b[0], b[3], b[1], b[4]);
-    nodes[4 * i + 2] = make_float4(a[2], a[5], b[2], b[5]);
-    nodes[4 * i + 3] = make_float4(__int_as_float(c.x), __int_as_float(c.y), 0.0f, 0.0f);
-}
-
-__global__ void k_pack_tris(const float* __restrict__ verts, const uint32_t* __restrict__ sidx, int64_t n,
-                            float4* __restrict__ tris) {
-    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    uint32_t t = sidx[p];
-    const float* v = verts + 9 * (int64_t)t;
-    f3 v0 = ld3(v), e1 = ld3(v + 3) - v0, e2 = ld3(v + 6) - v0;
-    tris[3 * p + 0] = make_float4(v0.x, v0.y, v0.z, __int_as_float((int)t));
-    tris[3 * p + 1] = make_float4(e1.x, e1.y, e1.z, 0.0f);
-    tris[3 * p + 2] = make_float4(e2.x, e2.y, e2.z, 0.0f);
-}
-
-struct BuildWork {
-    uint64_t *keys, *keys2;
-    uint32_t *idx, *idx2;
-    int2* child;
-    int32_t *parent_int, *parent_leaf, *flags;
-    float *leafbox, *intbox;
-    void* cub_tmp;
-    size_t cub_bytes;
-};
-
-static size_t build_layout(int64_t n, char* base, BuildWork* w) {
-    Bump b{base};
-    w->keys = b.take<uint64_t>(n);
-    w->keys2 = b.take<uint64_t>(n);
-    w->idx = b.take<uint32_t>(n);
-    w->idx2 = b.take<uint32_t>(n);
-    w->child = b.take<int2>(n);
-    w->parent_int = b.take<int32_t>(n);
-    w->parent_leaf = b.take<int32_t>(n);
-    w->flags = b.take<int32_t>(n);
-    w->leafbox = b.take<float>(6 * n);
-    w->intbox = b.take<float>(6 * n);
-    size_t cub = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, cub, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
-                                    (uint32_t*)nullptr, (int)n, 0, 64);
-    w->cub_bytes = cub;
-    w->cub_tmp = b.take<char>(cub);
-    return b.off;
-}
-
 static inline int blocks_for(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 }  // namespace vplgi
@@ -374,53 +207,6 @@ int32_t vpl_classify_near_far(const void* d_scene, double T, uint8_t* d_labels, 
     int grid = min(blocks_for(hh.n, 256), 148 * 8);
     k_classify<<<grid, 256, 0, s>>>(sv.hdr, sv.cen, hh.n, T2, d_labels, cnt);
     VPL_LAUNCHED("k_classify");
-    return VPL_OK;
-}
-
-int32_t vpl_bvh_bytes(int64_t n_tris, size_t* bvh_bytes, size_t* work_bytes) {
-    if (!bvh_bytes || !work_bytes || n_tris <= 0) return VPL_EINVAL;
-    *bvh_bytes = bvh_layout(n_tris, nullptr);
-    BuildWork w;
-    *work_bytes = build_layout(n_tris, nullptr, &w);
-    return VPL_OK;
-}
-
-int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* d_work, size_t work_bytes,
-                      void* stream) {
-    if (!d_scene || !d_bvh || !d_work) { set_error("vpl_build_bvh: null pointer"); return VPL_EINVAL; }
-    cudaStream_t s = (cudaStream_t)stream;
-    SceneHdr hh;
-    VPL_TRY(read_scene_hdr(d_scene, s, &hh));
-    int64_t n = hh.n;
-    size_t nb = 0, wb = 0;
-    VPL_TRY(vpl_bvh_bytes(n, &nb, &wb));
-    if (bvh_bytes < nb || work_bytes < wb) { set_error("vpl_build_bvh: buffers too small"); return VPL_ESMALL; }
-    SceneView sv = scene_view(d_scene, n);
-    BvhHdr bh;
-    bvh_layout(n, &bh);
-    VPL_CUDA(cudaMemcpyAsync(d_bvh, &bh, sizeof(bh), cudaMemcpyHostToDevice, s));
-    float4* nodes = (float4*)((char*)d_bvh + bh.off_nodes);
-    float4* tris = (float4*)((char*)d_bvh + bh.off_tris);
-    BuildWork w;
-    build_layout(n, (char*)d_work, &w);
-    k_morton63<<<blocks_for(n, 256), 256, 0, s>>>(sv.hdr, sv.cen, n, w.keys, w.idx);
-    VPL_LAUNCHED("k_morton63");
-    size_t cb = w.cub_bytes;
-    VPL_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, cb, w.keys, w.keys2, w.idx, w.idx2, (int)n, 0, 64, s));
-    if (n > 1) {
-        VPL_CUDA(cudaMemsetAsync(w.flags, 0, sizeof(int32_t) * n, s));
-        k_karras<<<blocks_for(n - 1, 256), 256, 0, s>>>(w.keys2, n, w.child, w.parent_int, w.parent_leaf);
-        VPL_LAUNCHED("k_karras");
-    }
-    k_refit<<<blocks_for(n, 256), 256, 0, s>>>(sv.hdr, sv.verts, w.idx2, n, w.child, w.parent_int, w.parent_leaf,
-                                               w.flags, w.leafbox, w.intbox);
-    VPL_LAUNCHED("k_refit");
-    if (n > 1) {
-        k_pack_nodes<<<blocks_for(n - 1, 256), 256, 0, s>>>(n, w.child, w.leafbox, w.intbox, nodes);
-        VPL_LAUNCHED("k_pack_nodes");
-    }
-    k_pack_tris<<<blocks_for(n, 256), 256, 0, s>>>(sv.verts, w.idx2, n, tris);
-    VPL_LAUNCHED("k_pack_tris");
     return VPL_OK;
 }
 
