@@ -9,6 +9,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <climits>
+
 #include "common.cuh"
 
 namespace vplgi {
@@ -147,7 +149,7 @@ __global__ void k_ploc_merge(const float4* __restrict__ cl, const int* __restric
 __global__ void k_sah_collapse(int64_t n, const int2* __restrict__ child, const float4* __restrict__ nbox,
                                const float4* __restrict__ lbox, const int* __restrict__ parent_int,
                                const int* __restrict__ parent_leaf, int* __restrict__ flags, int* __restrict__ cnt,
-                               float* __restrict__ cost, uint8_t* __restrict__ collapsed) {
+                               float* __restrict__ cost, uint8_t* __restrict__ collapsed, int* __restrict__ icount) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= n) return;
     int node = parent_leaf[p];
@@ -156,7 +158,7 @@ __global__ void k_sah_collapse(int64_t n, const int2* __restrict__ child, const 
         if (atomicAdd(&flags[node], 1) == 0) return;
         __threadfence();
         int2 c = child[node];
-        int cn[2];
+        int cn[2], ci[2];
         float cc[2], ca[2];
         int refs[2] = {c.x, c.y};
 #pragma unroll
@@ -165,9 +167,11 @@ __global__ void k_sah_collapse(int64_t n, const int2* __restrict__ child, const 
             if (r >= 0) {
                 cn[k] = __ldcg(cnt + r);
                 cc[k] = __ldcg(cost + r);
+                ci[k] = __ldcg(icount + r);
                 ca[k] = half_area(nbox[2 * r], nbox[2 * r + 1]);
             } else {
                 cn[k] = 1;
+                ci[k] = 0;
                 cc[k] = kCostTri;
                 ca[k] = half_area(lbox[2 * (~r)], lbox[2 * (~r) + 1]);
             }
@@ -179,6 +183,7 @@ __global__ void k_sah_collapse(int64_t n, const int2* __restrict__ child, const 
         bool col = total <= kMaxLeaf && c_leaf <= c_int && node != 0;
         __stcg(cnt + node, total);
         __stcg(cost + node, col ? c_leaf : c_int);
+        __stcg(icount + node, col ? 0 : 1 + ci[0] + ci[1]);
         collapsed[node] = col;
         node = parent_int[node];
     }
@@ -187,31 +192,40 @@ __global__ void k_sah_collapse(int64_t n, const int2* __restrict__ child, const 
 // depth-first triangle offset of every node (leaves: index ~p -> slot n-1+p)
 __global__ void k_dfs_offsets(int64_t n, const int2* __restrict__ child, const int* __restrict__ parent_int,
                               const int* __restrict__ parent_leaf, const int* __restrict__ cnt, int* __restrict__ off,
-                              int* __restrict__ max_depth) {
+                              int* __restrict__ max_depth, const int* __restrict__ icount,
+                              const uint8_t* __restrict__ collapsed, int* __restrict__ pre, uint8_t* __restrict__ hidden) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= 2 * n - 1) return;
     int self = k < n - 1 ? (int)k : ~(int)(k - (n - 1));
     int node = self;
     int par = node >= 0 ? parent_int[node] : parent_leaf[~node];
-    int o = 0, depth = 0;
+    int o = 0, depth = 0, pr = 0;
+    bool hid = false;
     while (par >= 0) {
         int2 c = child[par];
-        if (c.y == node) o += c.x >= 0 ? cnt[c.x] : 1;
+        if (c.y == node) {
+            o += c.x >= 0 ? cnt[c.x] : 1;
+            pr += c.x >= 0 ? icount[c.x] : 0;
+        }
+        pr += 1;
+        hid |= collapsed[par] != 0;
         node = par;
         par = parent_int[node];
         ++depth;
     }
     off[k] = o;
     if (self < 0) atomicMax(max_depth, depth);
+    else { pre[self] = pr; hidden[self] = hid; }
 }
 
 __device__ __forceinline__ int leaf_ref(int first, int count) { return ~((first << 3) | (count - 1)); }
 
 __global__ void k_emit_nodes(int64_t n, const int2* __restrict__ child, const float4* __restrict__ nbox,
                              const float4* __restrict__ lbox, const int* __restrict__ cnt, const int* __restrict__ off,
-                             const uint8_t* __restrict__ collapsed, float4* __restrict__ nodes) {
+                             const uint8_t* __restrict__ collapsed, const int* __restrict__ pre,
+                             const uint8_t* __restrict__ hidden, float4* __restrict__ nodes) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n - 1 || collapsed[i]) return;
+    if (i >= n - 1 || collapsed[i] || hidden[i]) return;
     int2 c = child[i];
     int refs[2] = {c.x, c.y};
     float4 lo[2], hi[2];
@@ -221,7 +235,7 @@ __global__ void k_emit_nodes(int64_t n, const int2* __restrict__ child, const fl
         int r = refs[k];
         if (r >= 0) {
             lo[k] = nbox[2 * r]; hi[k] = nbox[2 * r + 1];
-            out[k] = collapsed[r] ? leaf_ref(off[r], cnt[r]) : r;
+            out[k] = collapsed[r] ? leaf_ref(off[r], cnt[r]) : pre[r];
         } else {
             lo[k] = lbox[2 * (~r)]; hi[k] = lbox[2 * (~r) + 1];
             out[k] = leaf_ref(off[(n - 1) + (~r)], 1);
@@ -239,10 +253,125 @@ __global__ void k_emit_nodes(int64_t n, const int2* __restrict__ child, const fl
         lo[0] = lo[1]; hi[0] = hi[1]; lo[1] = tl; hi[1] = th;
         int to = out[0]; out[0] = out[1]; out[1] = to;
     }
-    nodes[4 * i + 0] = make_float4(lo[0].x, hi[0].x, lo[0].y, hi[0].y);
-    nodes[4 * i + 1] = make_float4(lo[1].x, hi[1].x, lo[1].y, hi[1].y);
-    nodes[4 * i + 2] = make_float4(lo[0].z, hi[0].z, lo[1].z, hi[1].z);
-    nodes[4 * i + 3] = make_float4(__int_as_float(out[0]), __int_as_float(out[1]), __int_as_float(axis), 0.0f);
+    int64_t s = pre[i];  // depth-first preorder slot (root = 0, first child adjacent)
+    nodes[4 * s + 0] = make_float4(lo[0].x, hi[0].x, lo[0].y, hi[0].y);
+    nodes[4 * s + 1] = make_float4(lo[1].x, hi[1].x, lo[1].y, hi[1].y);
+    nodes[4 * s + 2] = make_float4(lo[0].z, hi[0].z, lo[1].z, hi[1].z);
+    nodes[4 * s + 3] = make_float4(__int_as_float(out[0]), __int_as_float(out[1]), __int_as_float(axis), 0.0f);
+}
+
+
+// ---------------------------------------------------------------- kWide-wide collapse (BFS levels)
+__device__ __forceinline__ bool is_inner(int r, const uint8_t* __restrict__ collapsed) { return r >= 0 && !collapsed[r]; }
+
+__device__ __forceinline__ void ref_box(int r, const float4* __restrict__ nbox, const float4* __restrict__ lbox,
+                                        float4& lo, float4& hi) {
+    if (r >= 0) { lo = nbox[2 * r]; hi = nbox[2 * r + 1]; }
+    else { lo = lbox[2 * (~r)]; hi = lbox[2 * (~r) + 1]; }
+}
+
+// greedy: open the inner child of largest surface area until kWide children
+__global__ void k_wide_expand(const int* __restrict__ F, int nF, const int2* __restrict__ child,
+                              const float4* __restrict__ nbox, const uint8_t* __restrict__ collapsed,
+                              int* __restrict__ exp, int* __restrict__ nint) {
+    int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nF) return;
+    int b = F[f];
+    int ref[kWide];
+    int2 c = child[b];
+    ref[0] = c.x; ref[1] = c.y;
+    int cntc = 2;
+    while (cntc < kWide) {
+        int best = -1;
+        float ba = -1.0f;
+        for (int k = 0; k < cntc; ++k)
+            if (is_inner(ref[k], collapsed)) {
+                float a = half_area(nbox[2 * ref[k]], nbox[2 * ref[k] + 1]);
+                if (a > ba) { ba = a; best = k; }
+            }
+        if (best < 0) break;
+        int2 cc = child[ref[best]];
+        ref[best] = cc.x;
+        ref[cntc++] = cc.y;
+    }
+    int ni = 0;
+    for (int k = 0; k < kWide; ++k) {
+        int r = k < cntc ? ref[k] : INT_MIN;
+        exp[f * kWide + k] = r;
+        ni += (k < cntc && is_inner(r, collapsed)) ? 1 : 0;
+    }
+    nint[f] = ni;
+}
+
+__global__ void k_wide_write(const int* __restrict__ F, int nF, const int* __restrict__ exp,
+                             const int* __restrict__ nint, const int* __restrict__ noff, int base_cur, int base_next,
+                             const float4* __restrict__ nbox, const float4* __restrict__ lbox,
+                             const uint8_t* __restrict__ collapsed, const int* __restrict__ cnt,
+                             const int* __restrict__ toff, int64_t n, int* __restrict__ Fnext, float4* __restrict__ wide,
+                             int* __restrict__ total) {
+    int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nF) return;
+    if (f == nF - 1) *total = noff[f] + nint[f];
+    int b = F[f];
+    float4 L = nbox[2 * b], H = nbox[2 * b + 1];
+    float ex = H.x - L.x, ey = H.y - L.y, ez = H.z - L.z;
+    int axis = (ex >= ey && ex >= ez) ? 0 : (ey >= ez ? 1 : 2);
+    int ref[kWide];
+    float key[kWide];
+    float4 lo[kWide], hi[kWide];
+    int cntc = 0;
+    for (int k = 0; k < kWide; ++k) {
+        int r = exp[f * kWide + k];
+        if (r == INT_MIN) continue;
+        ref[cntc] = r;
+        ref_box(r, nbox, lbox, lo[cntc], hi[cntc]);
+        key[cntc] = axis == 0 ? lo[cntc].x + hi[cntc].x : axis == 1 ? lo[cntc].y + hi[cntc].y : lo[cntc].z + hi[cntc].z;
+        ++cntc;
+    }
+    // insertion sort by centre along axis (stable)
+    for (int i = 1; i < cntc; ++i)
+        for (int j = i; j > 0 && key[j] < key[j - 1]; --j) {
+            float tk = key[j]; key[j] = key[j - 1]; key[j - 1] = tk;
+            int tr = ref[j]; ref[j] = ref[j - 1]; ref[j - 1] = tr;
+            float4 tl = lo[j]; lo[j] = lo[j - 1]; lo[j - 1] = tl;
+            float4 th = hi[j]; hi[j] = hi[j - 1]; hi[j - 1] = th;
+        }
+    float q[6][kWide];
+    int out[kWide];
+    int j = 0;
+    // centre / half-extent form (packet slab test on the FMA pipe); the half extent is
+    // widened by 2^-20 * max|coord| so rounding of c and e keeps the box conservative.
+    // Empty slots are masked by the child count stored in the meta word.
+    for (int k = 0; k < kWide; ++k) {
+        if (k >= cntc) {
+            for (int a = 0; a < 6; ++a) q[a][k] = 0.0f;
+            out[k] = INT_MIN;
+            continue;
+        }
+        int r = ref[k];
+        float l3[3] = {lo[k].x, lo[k].y, lo[k].z}, h3[3] = {hi[k].x, hi[k].y, hi[k].z};
+        for (int a = 0; a < 3; ++a) {
+            float m = fmaxf(fabsf(l3[a]), fabsf(h3[a]));
+            q[2 * a][k] = 0.5f * (l3[a] + h3[a]);
+            q[2 * a + 1][k] = 0.5f * (h3[a] - l3[a]) + m * 0x1p-20f;
+        }
+        if (is_inner(r, collapsed)) {
+            int slot = noff[f] + j++;
+            Fnext[slot] = r;
+            out[k] = base_next + slot;
+        } else if (r >= 0) {
+            out[k] = leaf_ref(toff[r], cnt[r]);
+        } else {
+            out[k] = leaf_ref(toff[(n - 1) + (~r)], 1);
+        }
+    }
+    float4* w = wide + (int64_t)kWideF4 * (base_cur + f);
+    for (int a = 0; a < 6; ++a)
+        for (int k = 0; k < kWide; k += 4) w[a * (kWide / 4) + k / 4] = make_float4(q[a][k], q[a][k + 1], q[a][k + 2], q[a][k + 3]);
+    for (int k = 0; k < kWide; k += 4)
+        w[6 * (kWide / 4) + k / 4] = make_float4(__int_as_float(out[k]), __int_as_float(out[k + 1]),
+                                                 __int_as_float(out[k + 2]), __int_as_float(out[k + 3]));
+    w[kWideF4 - 1] = make_float4(__int_as_float(axis), __int_as_float((1 << cntc) - 1), 0.0f, 0.0f);  // axis, valid-slot mask
 }
 
 __global__ void k_emit_tris(const float* __restrict__ verts, const uint32_t* __restrict__ sidx, int64_t n,
@@ -262,7 +391,9 @@ struct BuildWork {
     uint64_t *keys, *keys2;
     uint32_t *idx, *idx2;
     float4 *clA, *clB, *lbox, *nbox;
-    int *nn, *parent_int, *parent_leaf, *flags, *cnt, *off, *totals;
+    int *nn, *parent_int, *parent_leaf, *flags, *cnt, *off, *totals, *icount, *pre;
+    uint8_t* hidden;
+    int *F0, *F1, *wexp, *nint, *noff;
     unsigned long long *mflags, *moff;
     float* cost;
     uint8_t* collapsed;
@@ -292,12 +423,23 @@ static size_t build_layout(int64_t n, char* base, BuildWork* w) {
     w->moff = b.take<unsigned long long>(n);
     w->cost = b.take<float>(n);
     w->collapsed = b.take<uint8_t>(n);
+    w->icount = b.take<int>(n);
+    w->pre = b.take<int>(n);
+    w->hidden = b.take<uint8_t>(n);
+    w->F0 = b.take<int>(n);
+    w->F1 = b.take<int>(n);
+    w->wexp = b.take<int>((size_t)kWide * n);
+    w->nint = b.take<int>(n);
+    w->noff = b.take<int>(n);
     w->child = b.take<int2>(n);
     size_t c1 = 0, c2 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, c1, (uint64_t*)nullptr, (uint64_t*)nullptr, (uint32_t*)nullptr,
                                     (uint32_t*)nullptr, (int)n, 0, 64);
     cub::DeviceScan::ExclusiveSum(nullptr, c2, (unsigned long long*)nullptr, (unsigned long long*)nullptr, (int)n);
+    size_t c3 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, c3, (int*)nullptr, (int*)nullptr, (int)n);
     w->cub_bytes = c1 > c2 ? c1 : c2;
+    if (c3 > w->cub_bytes) w->cub_bytes = c3;
     w->cub = b.take<char>(w->cub_bytes);
     return b.off;
 }
@@ -371,14 +513,36 @@ int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* 
         // SAH collapse, depth-first ordering, emission
         VPL_CUDA(cudaMemsetAsync(w.flags, 0, sizeof(int) * n, s));
         k_sah_collapse<<<nblk(n, 256), 256, 0, s>>>(n, w.child, w.nbox, w.lbox, w.parent_int, w.parent_leaf, w.flags,
-                                                    w.cnt, w.cost, w.collapsed);
+                                                    w.cnt, w.cost, w.collapsed, w.icount);
         VPL_LAUNCHED("k_sah_collapse");
         VPL_CUDA(cudaMemsetAsync(w.totals + 2, 0, sizeof(int), s));
         k_dfs_offsets<<<nblk(2 * n - 1, 256), 256, 0, s>>>(n, w.child, w.parent_int, w.parent_leaf, w.cnt, w.off,
-                                                           w.totals + 2);
+                                                           w.totals + 2, w.icount, w.collapsed, w.pre, w.hidden);
         VPL_LAUNCHED("k_dfs_offsets");
-        k_emit_nodes<<<nblk(n - 1, 256), 256, 0, s>>>(n, w.child, w.nbox, w.lbox, w.cnt, w.off, w.collapsed, nodes);
+        k_emit_nodes<<<nblk(n - 1, 256), 256, 0, s>>>(n, w.child, w.nbox, w.lbox, w.cnt, w.off, w.collapsed, w.pre,
+                                                       w.hidden, nodes);
         VPL_LAUNCHED("k_emit_nodes");
+        // kWide-wide nodes for the packet traversal, breadth-first from the root
+        float4* wide = (float4*)((char*)d_bvh + bh.off_wide);
+        int zero = 0;
+        VPL_CUDA(cudaMemcpyAsync(w.F0, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+        int nF = 1, base = 0;
+        int *Fc = w.F0, *Fn = w.F1;
+        while (nF > 0) {
+            k_wide_expand<<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.child, w.nbox, w.collapsed, w.wexp, w.nint);
+            VPL_LAUNCHED("k_wide_expand");
+            cb = w.cub_bytes;
+            VPL_CUDA(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.nint, w.noff, nF, s));
+            k_wide_write<<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.wexp, w.nint, w.noff, base, base + nF, w.nbox, w.lbox,
+                                                       w.collapsed, w.cnt, w.off, n, Fn, wide, w.totals + 3);
+            VPL_LAUNCHED("k_wide_write");
+            int next = 0;
+            VPL_CUDA(cudaMemcpyAsync(&next, w.totals + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
+            VPL_CUDA(cudaStreamSynchronize(s));
+            base += nF;
+            nF = next;
+            int* t = Fc; Fc = Fn; Fn = t;
+        }
     }
     k_emit_tris<<<nblk(n, 256), 256, 0, s>>>(sv.verts, w.idx2, n, w.off, tris);
     VPL_LAUNCHED("k_emit_tris");

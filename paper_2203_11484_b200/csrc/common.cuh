@@ -84,22 +84,31 @@ inline SceneView scene_view(const void* blob, int64_t n) {
 
 // BVH blob = BvhHdr, internal nodes (4 float4 each), leaf-ordered triangles
 // (3 float4 each: v0 | orig index bits, e1, e2).
+// kWide-wide node (packet traversal): SoA child boxes as centre / half extent
+// c.x[W] e.x[W] c.y[W] e.y[W] c.z[W] e.z[W], child refs[W], meta (axis,
+// n_children); children sorted by centre along `axis`, empty slots last.
+constexpr int kWide = 4;
+constexpr int kWideF4 = (6 * kWide + kWide) / 4 + 1;  // float4s per wide node (8 for W = 4)
+
 struct BvhHdr {
     int64_t n;
     int32_t root;       // 0 (internal) or ~0 (single leaf)
     int32_t pad;
-    int64_t off_nodes, off_tris;
+    int64_t off_nodes, off_tris, off_wide;
 };
 struct BvhView {
-    const float4* nodes;
+    const float4* nodes;   // binary nodes (per-thread traversals)
     const float4* tris;
+    const float4* wide;    // kWide-wide nodes (packet traversal)
     int32_t root;
 };
 inline size_t bvh_layout(int64_t n, BvhHdr* h) {
     size_t off = align_up(sizeof(BvhHdr));
-    size_t o_n = off; off = align_up(off + sizeof(float4) * 4 * (size_t)(n > 1 ? n - 1 : 1));
+    size_t ni = (size_t)(n > 1 ? n - 1 : 1);
+    size_t o_n = off; off = align_up(off + sizeof(float4) * 4 * ni);
     size_t o_t = off; off = align_up(off + sizeof(float4) * 3 * (size_t)n);
-    if (h) { h->n = n; h->root = n > 1 ? 0 : ~0; h->off_nodes = o_n; h->off_tris = o_t; }
+    size_t o_w = off; off = align_up(off + sizeof(float4) * kWideF4 * ni);
+    if (h) { h->n = n; h->root = n > 1 ? 0 : ~0; h->off_nodes = o_n; h->off_tris = o_t; h->off_wide = o_w; }
     return off;
 }
 inline BvhView bvh_view(const void* blob, int64_t n) {
@@ -108,6 +117,7 @@ inline BvhView bvh_view(const void* blob, int64_t n) {
     BvhView v;
     v.nodes = (const float4*)((const char*)blob + h.off_nodes);
     v.tris = (const float4*)((const char*)blob + h.off_tris);
+    v.wide = (const float4*)((const char*)blob + h.off_wide);
     v.root = h.root;
     return v;
 }
@@ -239,6 +249,7 @@ __device__ __forceinline__ void leaf_range(int node, int& first, int& count) {
 }
 
 constexpr int kStack = 128;  // > max tree depth, checked at build time (vpl_build_bvh)
+constexpr int kWarpStack = 3 * kStack;  // wide traversal pushes up to kWide-1 per level
 
 // Any hit in (tmin, tmax), one ray per thread.
 template <bool kCount>
@@ -342,55 +353,64 @@ __device__ __forceinline__ bool segment_occluded(const BvhView& bv, f3 a, f3 b, 
     return bvh_any_hit<kCount>(bv, r, st);
 }
 
-// Warp-cooperative any-hit (packet traversal): the 32 lanes carry their own
-// rays but walk ONE node sequence — a child is entered if any live lane's ray
-// enters its box — so node and triangle fetches are warp-uniform broadcasts
-// and the traversal stack is warp-uniform (shared memory, one slot per level).
-// A lane may test triangles its own boxes would have culled; that cannot
-// change an any-hit result, so each lane's answer equals bvh_any_hit's.
-// Children are visited in the order of the node's split axis and the packet
-// leader's direction sign (dir_neg bit a = leader's dir[a] < 0).
-// `cache` (in/out, per lane): leaf-order index of the last occluder found; it
-// is tested first (exact MT), which resolves coherent occluded rays without a
-// traversal.  Must be called by all 32 lanes with the same sstack.
-template <bool kCount>
-__device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, bool live, int& cache,
-                                             int* __restrict__ sstack, TravStats* st) {
-    bool occl = false;
-    if (live && cache >= 0) {
-        const float4* tr = bv.tris + 3 * cache;
-        float t;
-        if (kCount) st->tris += 1;
-        occl = mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t);
+// Packet slab test on a wide-node child in centre / half-extent form:
+// t = (c - o) * idir -+ e * |idir| per axis — 12 FMA-pipe ops and 5 ALU ops,
+// independent of the ray's direction signs (no per-axis min/max).
+__device__ __forceinline__ bool slab_ce(const Ray& r, f3 aidir, float cx, float ex, float cy, float ey, float cz,
+                                        float ez) {
+    float ux = fmaf(cx, r.idir.x, -r.ood.x), vx = ex * aidir.x;
+    float uy = fmaf(cy, r.idir.y, -r.ood.y), vy = ey * aidir.y;
+    float uz = fmaf(cz, r.idir.z, -r.ood.z), vz = ez * aidir.z;
+    float tn = fmax3(ux - vx, uy - vy, fmaxf(uz - vz, r.tmin));
+    float tf = fmin3(ux + vx, uy + vy, fminf(uz + vz, r.tmax));
+    return tn <= tf;
+}
+
+struct OccluderCache {
+    int own0 = -1, own1 = -1;  // this lane's two most recent occluders (leaf-order triangle index)
+    int warp = -1;             // the warp's most recent occluder (uniform)
+    __device__ __forceinline__ void found(int tri) {
+        if (tri != own0) { own1 = own0; own0 = tri; }
     }
-    unsigned need = __ballot_sync(0xFFFFFFFFu, live && !occl);
-    if (!need) return occl;
-    int leader = __ffs(need) - 1;
-    unsigned neg = (r.d.x < 0.0f ? 1u : 0u) | (r.d.y < 0.0f ? 2u : 0u) | (r.d.z < 0.0f ? 4u : 0u);
-    const unsigned dir_neg = __shfl_sync(0xFFFFFFFFu, neg, leader);
-    if (kCount && (threadIdx.x & 31) == 0) st->wrays += 1;
+};
+
+template <bool kCount>
+__device__ __forceinline__ bool warp_traverse(const BvhView& bv, const Ray& r, bool live, bool occl,
+                                              OccluderCache& cache, unsigned dir_neg, int* __restrict__ sstack,
+                                              TravStats* st) {
+    const f3 aidir = mk3(fabsf(r.idir.x), fabsf(r.idir.y), fabsf(r.idir.z));
     int sp = 0;
     int node = bv.root;
     while (true) {
         const bool go = live && !occl;
         if (kCount && (threadIdx.x & 31) == 0) st->wsteps += 1;
         if (node >= 0) {
-            const float4* nd = bv.nodes + 4 * node;
-            float4 n0 = __ldg(nd + 0), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
-            float t0, t1;
-            bool h0 = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, r.tmax, t0) & go;
-            bool h1 = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, r.tmax, t1) & go;
-            if (kCount && go) st->boxes += 2;
-            unsigned b0 = __ballot_sync(0xFFFFFFFFu, h0), b1 = __ballot_sync(0xFFFFFFFFu, h1);
-            int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
-            if (b0 | b1) {
-                if (b0 && b1) {
-                    bool rev = (dir_neg >> __float_as_int(n3.z)) & 1u;
-                    sstack[sp++] = rev ? c0 : c1;
-                    node = rev ? c1 : c0;
-                } else {
-                    node = b0 ? c0 : c1;
+            const float4* nd = bv.wide + kWideF4 * node;
+            float4 cx = __ldg(nd + 0), ex = __ldg(nd + 1), cy = __ldg(nd + 2), ey = __ldg(nd + 3);
+            float4 cz = __ldg(nd + 4), ez = __ldg(nd + 5), rf = __ldg(nd + 6), mt = __ldg(nd + 7);
+            bool h0 = slab_ce(r, aidir, cx.x, ex.x, cy.x, ey.x, cz.x, ez.x) & go;
+            bool h1 = slab_ce(r, aidir, cx.y, ex.y, cy.y, ey.y, cz.y, ez.y) & go;
+            bool h2 = slab_ce(r, aidir, cx.z, ex.z, cy.z, ey.z, cz.z, ez.z) & go;
+            bool h3 = slab_ce(r, aidir, cx.w, ex.w, cy.w, ey.w, cz.w, ez.w) & go;
+            if (kCount && go) st->boxes += 4;
+            unsigned lm = (h0 ? 1u : 0u) | (h1 ? 2u : 0u) | (h2 ? 4u : 0u) | (h3 ? 8u : 0u);
+            unsigned m = __reduce_or_sync(0xFFFFFFFFu, lm) & (unsigned)__float_as_int(mt.y);  // valid-slot mask
+            if (m) {
+                int r0 = __float_as_int(rf.x), r1 = __float_as_int(rf.y), r2 = __float_as_int(rf.z),
+                    r3 = __float_as_int(rf.w);
+                // visit order: stored order (ascending centre along axis), reversed for a -axis packet
+                if ((dir_neg >> __float_as_int(mt.x)) & 1u) {
+                    m = __brev(m) >> 28;
+                    int t0 = r0, t1 = r1;
+                    r0 = r3; r1 = r2; r2 = t1; r3 = t0;
                 }
+                int first = (m & 1u) ? r0 : (m & 2u) ? r1 : (m & 4u) ? r2 : r3;
+                unsigned rest = m & (m - 1u);
+                // push the later hits, farthest first, so the next in order is on top
+                if (rest & 8u) sstack[sp++] = r3;
+                if (rest & 4u) sstack[sp++] = r2;
+                if (rest & 2u) sstack[sp++] = r1;
+                node = first;
                 continue;
             }
         } else {
@@ -402,13 +422,58 @@ __device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, bo
                 float t;
                 bool hit = mt_hit(r.o, r.d, a, b, c, r.tmin, r.tmax, t) & go & !occl;
                 if (kCount && go && !occl) st->tris += 1;
-                if (hit) { occl = true; cache = first + k; }
+                if (hit) { occl = true; cache.found(first + k); }
             }
             if (!__any_sync(0xFFFFFFFFu, live && !occl)) break;
         }
         if (sp == 0) break;
         node = sstack[--sp];
     }
+    return occl;
+}
+
+// Warp-cooperative any-hit (packet traversal): the 32 lanes carry their own
+// rays but walk ONE node sequence — a child is entered if any live lane's ray
+// enters its box — so node and triangle fetches are warp-uniform broadcasts
+// and the traversal stack is warp-uniform (shared memory, one slot per level).
+// A lane may test triangles its own boxes would have culled; that cannot
+// change an any-hit result, so each lane's answer equals bvh_any_hit's.
+// Children are visited in the order of the node's split axis and the packet
+// leader's direction sign.
+// `cache` (in/out, per lane): leaf-order index of the last occluder found; it
+// is tested first (exact MT), which resolves coherent occluded rays without a
+// traversal.  Must be called by all 32 lanes with the same sstack.
+template <bool kCount>
+__device__ __forceinline__ bool cached_occluder(const BvhView& bv, const Ray& r, int tri, TravStats* st) {
+    const float4* tr = bv.tris + 3 * tri;
+    float t;
+    if (kCount) st->tris += 1;
+    return mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t);
+}
+
+template <bool kCount>
+__device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, bool live, OccluderCache& cache,
+                                             int* __restrict__ sstack, TravStats* st) {
+    // exact MT tests of recently found occluders resolve coherent occluded rays
+    // without a traversal (consecutive VPLs are spatially coherent: Morton order)
+    bool occl = false;
+    if (live && cache.own0 >= 0) occl = cached_occluder<kCount>(bv, r, cache.own0, st);
+    if (live && !occl && cache.own1 >= 0) occl = cached_occluder<kCount>(bv, r, cache.own1, st);
+    if (live && !occl && cache.warp >= 0 && cache.warp != cache.own0 && cache.warp != cache.own1) {
+        occl = cached_occluder<kCount>(bv, r, cache.warp, st);
+        if (occl) cache.found(cache.warp);
+    }
+    unsigned need = __ballot_sync(0xFFFFFFFFu, live && !occl);
+    if (!need) return occl;
+    int leader = __ffs(need) - 1;
+    unsigned neg = (r.d.x < 0.0f ? 1u : 0u) | (r.d.y < 0.0f ? 2u : 0u) | (r.d.z < 0.0f ? 4u : 0u);
+    const unsigned dir_neg = __shfl_sync(0xFFFFFFFFu, neg, leader);
+    if (kCount && (threadIdx.x & 31) == 0) st->wrays += 1;
+    bool was = occl;
+    occl = warp_traverse<kCount>(bv, r, live, occl, cache, dir_neg, sstack, st);
+    // share the newest occluder found in this traversal with the whole warp
+    unsigned fresh = __ballot_sync(0xFFFFFFFFu, occl && !was);
+    if (fresh) cache.warp = __shfl_sync(0xFFFFFFFFu, cache.own0, __ffs(fresh) - 1);
     return occl;
 }
 

@@ -44,6 +44,19 @@ __global__ void k_gbuffer(SceneView sv, BvhView bv, TileMap tm, vpl_gpoint* __re
     gb[pix] = o;
 }
 
+struct VplPos {
+    f3 y, n;
+    int tri;
+};
+__device__ __forceinline__ VplPos load_vpl_geo(const vpl_record* v) {
+    const float4* p = (const float4*)v;
+    float4 a = __ldg(p), b = __ldg(p + 1);
+    VplPos g;
+    g.y = xyz(a); g.tri = __float_as_int(a.w);
+    g.n = xyz(b);
+    return g;
+}
+
 struct VplGeo {
     f3 y, n, phi;
     int tri;
@@ -62,10 +75,10 @@ __device__ __forceinline__ VplGeo load_vpl(const vpl_record* v) {
 // end point (coherent traversal).  fp32 two-level accumulation: a per-batch
 // partial is folded into the running total every 256 VPLs.
 template <bool kCount>
-__global__ void __launch_bounds__(128) k_gather(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb,
+__global__ void __launch_bounds__(128, 8) k_gather(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb,
                                                 const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
                                                 vpl_counters* __restrict__ ctr, int* __restrict__ queue) {
-    __shared__ int s_stack[4][kStack];
+    __shared__ int s_stack[4][kWarpStack];
     const int lane = threadIdx.x & 31;
     int* sstack = s_stack[threadIdx.x >> 5];
     const int64_t nw = tm.n_warps();
@@ -77,17 +90,17 @@ __global__ void __launch_bounds__(128) k_gather(SceneView sv, BvhView bv, TileMa
         if (g >= nw) break;
         int32_t pix = tm.pixel(g, lane);
         bool active = false;
-        f3 x = mk3(0, 0, 0), nx = mk3(0, 0, 0), rho = mk3(0, 0, 0);
+        f3 x = mk3(0, 0, 0), nx = mk3(0, 0, 0);
         int tri_x = -1;
         if (pix >= 0) {
             const float4* gp = (const float4*)(gb + pix);
-            float4 a = gp[0], b = gp[1], c = gp[2];
+            float4 a = gp[0], b = gp[1];
             tri_x = __float_as_int(a.w);
             active = tri_x >= 0 && __float_as_int(b.w) != 0;
-            x = xyz(a); nx = xyz(b); rho = xyz(c);
+            x = xyz(a); nx = xyz(b);
         }
         float acc[3] = {0.0f, 0.0f, 0.0f};
-        int cache = -1;
+        OccluderCache cache;
         TravStats st;
         unsigned long long n_traced = 0, n_vis = 0;
         if (__any_sync(0xFFFFFFFFu, active)) {
@@ -95,7 +108,7 @@ __global__ void __launch_bounds__(128) k_gather(SceneView sv, BvhView bv, TileMa
                 float part[3] = {0.0f, 0.0f, 0.0f};
                 int i1 = min(M, i0 + 256);
                 for (int i = i0; i < i1; ++i) {
-                    VplGeo v = load_vpl(vpls + i);
+                    VplPos v = load_vpl_geo(vpls + i);
                     f3 d = v.y - x;
                     float r2 = dot(d, d);
                     float cx = dot(nx, d);
@@ -109,15 +122,17 @@ __global__ void __launch_bounds__(128) k_gather(SceneView sv, BvhView bv, TileMa
                     if (!traced || occl) continue;
                     if (kCount) ++n_vis;
                     float w = __fdividef(cx * ci, r2 * fmaxf(r2, b2));
-                    part[0] = fmaf(v.phi.x, w, part[0]);
-                    part[1] = fmaf(v.phi.y, w, part[1]);
-                    part[2] = fmaf(v.phi.z, w, part[2]);
+                    float4 phi = __ldg((const float4*)(vpls + i) + 2);
+                    part[0] = fmaf(phi.x, w, part[0]);
+                    part[1] = fmaf(phi.y, w, part[1]);
+                    part[2] = fmaf(phi.z, w, part[2]);
                 }
                 acc[0] += part[0]; acc[1] += part[1]; acc[2] += part[2];
             }
         }
         if (pix >= 0) {
             const float s = (float)(1.0 / kPiR);
+            f3 rho = xyz(((const float4*)(gb + pix))[2]);
             float* o = rgb + 3 * (int64_t)pix;
             o[0] = active ? acc[0] * rho.x * s : 0.0f;
             o[1] = active ? acc[1] * rho.y * s : 0.0f;
@@ -151,11 +166,11 @@ __global__ void __launch_bounds__(128) k_gather(SceneView sv, BvhView bv, TileMa
 __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict__ gb, const vpl_record* __restrict__ vpls,
                           int32_t M, const int32_t* __restrict__ pixels, int32_t n_px, uint32_t* __restrict__ tbits,
                           uint32_t* __restrict__ vbits) {
-    __shared__ int s_stack[2][kStack];
+    __shared__ int s_stack[2][kWarpStack];
     int* sstack = s_stack[threadIdx.x >> 5];
     int64_t words = (M + 31) / 32;
     int lane = threadIdx.x & 31;
-    int cache = -1;
+    OccluderCache cache;
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if ((k - lane) >= n_px) return;                      // whole warp out of range
     bool inb = k < n_px;
