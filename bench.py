@@ -249,7 +249,7 @@ def run_ours(args):
         peak_ops = sm_count * 128 * f_max                      # 4 SMSP x 32 lanes issue per clock
         ops = algorithmic_ops(ctr) / max(world, 1)              # per launch (one rank's share)
         achieved = ops / (t_gather * 1e-3)
-        pairs, traced, visible, boxes, tris, wrays, wsteps = (int(x) for x in ctr)
+        pairs, traced, visible, boxes, tris, wrays, wsteps = (int(x) for x in ctr[:7])
         out = {
             "metric": METRIC, "value": pairs_per_step / (t_step * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,

@@ -122,6 +122,7 @@ typedef struct {
     unsigned long long tri_tests;  /* Moller-Trumbore tests */
     unsigned long long warp_rays;  /* warp-level shadow-ray packets (>= 1 traced lane) */
     unsigned long long warp_steps; /* warp-level traversal iterations (node or leaf visits) */
+    unsigned long long aux[4];     /* diagnostics (packet classes) */
 } vpl_counters;
 
 /* -------------------------------------------------------------------- */

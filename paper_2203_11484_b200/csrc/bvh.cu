@@ -271,17 +271,18 @@ __device__ __forceinline__ void ref_box(int r, const float4* __restrict__ nbox, 
 }
 
 // greedy: open the inner child of largest surface area until kWide children
+template <int kW>
 __global__ void k_wide_expand(const int* __restrict__ F, int nF, const int2* __restrict__ child,
                               const float4* __restrict__ nbox, const uint8_t* __restrict__ collapsed,
                               int* __restrict__ exp, int* __restrict__ nint) {
     int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f >= nF) return;
     int b = F[f];
-    int ref[kWide];
+    int ref[kW];
     int2 c = child[b];
     ref[0] = c.x; ref[1] = c.y;
     int cntc = 2;
-    while (cntc < kWide) {
+    while (cntc < kW) {
         int best = -1;
         float ba = -1.0f;
         for (int k = 0; k < cntc; ++k)
@@ -295,9 +296,9 @@ __global__ void k_wide_expand(const int* __restrict__ F, int nF, const int2* __r
         ref[cntc++] = cc.y;
     }
     int ni = 0;
-    for (int k = 0; k < kWide; ++k) {
+    for (int k = 0; k < kW; ++k) {
         int r = k < cntc ? ref[k] : INT_MIN;
-        exp[f * kWide + k] = r;
+        exp[f * kW + k] = r;
         ni += (k < cntc && is_inner(r, collapsed)) ? 1 : 0;
     }
     nint[f] = ni;
@@ -318,10 +319,67 @@ __global__ void k_wide_write(const int* __restrict__ F, int nF, const int* __res
     int axis = (ex >= ey && ex >= ez) ? 0 : (ey >= ez ? 1 : 2);
     int ref[kWide];
     float key[kWide];
-    float4 lo[kWide], hi[kWide];
     int cntc = 0;
     for (int k = 0; k < kWide; ++k) {
         int r = exp[f * kWide + k];
+        if (r == INT_MIN) continue;
+        float4 lo, hi;
+        ref_box(r, nbox, lbox, lo, hi);
+        ref[cntc] = r;
+        key[cntc] = axis == 0 ? lo.x + hi.x : axis == 1 ? lo.y + hi.y : lo.z + hi.z;
+        ++cntc;
+    }
+    // insertion sort by centre along axis (stable)
+    for (int i = 1; i < cntc; ++i)
+        for (int j = i; j > 0 && key[j] < key[j - 1]; --j) {
+            float tk = key[j]; key[j] = key[j - 1]; key[j - 1] = tk;
+            int tr = ref[j]; ref[j] = ref[j - 1]; ref[j - 1] = tr;
+        }
+    float4* w = wide + (int64_t)kWideF4 * (base_cur + f);
+    int j = 0;
+    for (int k = 0; k < kWide; ++k) {
+        if (k >= cntc) {
+            w[2 * k] = make_float4(0.0f, 0.0f, 0.0f, __int_as_float(INT_MIN));
+            w[2 * k + 1] = make_float4(0.0f, 0.0f, 0.0f, __int_as_float(axis));
+            continue;
+        }
+        int r = ref[k];
+        float4 lo, hi;
+        ref_box(r, nbox, lbox, lo, hi);
+        int out;
+        if (is_inner(r, collapsed)) {
+            int slot = noff[f] + j++;
+            Fnext[slot] = r;
+            out = base_next + slot;
+        } else if (r >= 0) {
+            out = leaf_ref(toff[r], cnt[r]);
+        } else {
+            out = leaf_ref(toff[(n - 1) + (~r)], 1);
+        }
+        w[2 * k] = make_float4(lo.x, lo.y, lo.z, __int_as_float(out));
+        w[2 * k + 1] = make_float4(hi.x, hi.y, hi.z, __int_as_float(axis));
+    }
+}
+
+__global__ void k_wide4_write(const int* __restrict__ F, int nF, const int* __restrict__ exp,
+                             const int* __restrict__ nint, const int* __restrict__ noff, int base_cur, int base_next,
+                             const float4* __restrict__ nbox, const float4* __restrict__ lbox,
+                             const uint8_t* __restrict__ collapsed, const int* __restrict__ cnt,
+                             const int* __restrict__ toff, int64_t n, int* __restrict__ Fnext, float4* __restrict__ wide,
+                             int* __restrict__ total) {
+    int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nF) return;
+    if (f == nF - 1) *total = noff[f] + nint[f];
+    int b = F[f];
+    float4 L = nbox[2 * b], H = nbox[2 * b + 1];
+    float ex = H.x - L.x, ey = H.y - L.y, ez = H.z - L.z;
+    int axis = (ex >= ey && ex >= ez) ? 0 : (ey >= ez ? 1 : 2);
+    int ref[kWide4];
+    float key[kWide4];
+    float4 lo[kWide4], hi[kWide4];
+    int cntc = 0;
+    for (int k = 0; k < kWide4; ++k) {
+        int r = exp[f * kWide4 + k];
         if (r == INT_MIN) continue;
         ref[cntc] = r;
         ref_box(r, nbox, lbox, lo[cntc], hi[cntc]);
@@ -336,13 +394,13 @@ __global__ void k_wide_write(const int* __restrict__ F, int nF, const int* __res
             float4 tl = lo[j]; lo[j] = lo[j - 1]; lo[j - 1] = tl;
             float4 th = hi[j]; hi[j] = hi[j - 1]; hi[j - 1] = th;
         }
-    float q[6][kWide];
-    int out[kWide];
+    float q[6][kWide4];
+    int out[kWide4];
     int j = 0;
     // centre / half-extent form (packet slab test on the FMA pipe); the half extent is
     // widened by 2^-20 * max|coord| so rounding of c and e keeps the box conservative.
     // Empty slots are masked by the child count stored in the meta word.
-    for (int k = 0; k < kWide; ++k) {
+    for (int k = 0; k < kWide4; ++k) {
         if (k >= cntc) {
             for (int a = 0; a < 6; ++a) q[a][k] = 0.0f;
             out[k] = INT_MIN;
@@ -365,14 +423,15 @@ __global__ void k_wide_write(const int* __restrict__ F, int nF, const int* __res
             out[k] = leaf_ref(toff[(n - 1) + (~r)], 1);
         }
     }
-    float4* w = wide + (int64_t)kWideF4 * (base_cur + f);
+    float4* w = wide + (int64_t)kWide4F4 * (base_cur + f);
     for (int a = 0; a < 6; ++a)
-        for (int k = 0; k < kWide; k += 4) w[a * (kWide / 4) + k / 4] = make_float4(q[a][k], q[a][k + 1], q[a][k + 2], q[a][k + 3]);
-    for (int k = 0; k < kWide; k += 4)
-        w[6 * (kWide / 4) + k / 4] = make_float4(__int_as_float(out[k]), __int_as_float(out[k + 1]),
+        for (int k = 0; k < kWide4; k += 4) w[a * (kWide4 / 4) + k / 4] = make_float4(q[a][k], q[a][k + 1], q[a][k + 2], q[a][k + 3]);
+    for (int k = 0; k < kWide4; k += 4)
+        w[6 * (kWide4 / 4) + k / 4] = make_float4(__int_as_float(out[k]), __int_as_float(out[k + 1]),
                                                  __int_as_float(out[k + 2]), __int_as_float(out[k + 3]));
-    w[kWideF4 - 1] = make_float4(__int_as_float(axis), __int_as_float((1 << cntc) - 1), 0.0f, 0.0f);  // axis, valid-slot mask
+    w[kWide4F4 - 1] = make_float4(__int_as_float(axis), __int_as_float((1 << cntc) - 1), 0.0f, 0.0f);  // axis, valid-slot mask
 }
+
 
 __global__ void k_emit_tris(const float* __restrict__ verts, const uint32_t* __restrict__ sidx, int64_t n,
                             const int* __restrict__ off, float4* __restrict__ tris) {
@@ -522,26 +581,41 @@ int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* 
         k_emit_nodes<<<nblk(n - 1, 256), 256, 0, s>>>(n, w.child, w.nbox, w.lbox, w.cnt, w.off, w.collapsed, w.pre,
                                                        w.hidden, nodes);
         VPL_LAUNCHED("k_emit_nodes");
-        // kWide-wide nodes for the packet traversal, breadth-first from the root
-        float4* wide = (float4*)((char*)d_bvh + bh.off_wide);
-        int zero = 0;
-        VPL_CUDA(cudaMemcpyAsync(w.F0, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
-        int nF = 1, base = 0;
-        int *Fc = w.F0, *Fn = w.F1;
-        while (nF > 0) {
-            k_wide_expand<<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.child, w.nbox, w.collapsed, w.wexp, w.nint);
-            VPL_LAUNCHED("k_wide_expand");
-            cb = w.cub_bytes;
-            VPL_CUDA(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.nint, w.noff, nF, s));
-            k_wide_write<<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.wexp, w.nint, w.noff, base, base + nF, w.nbox, w.lbox,
-                                                       w.collapsed, w.cnt, w.off, n, Fn, wide, w.totals + 3);
-            VPL_LAUNCHED("k_wide_write");
-            int next = 0;
-            VPL_CUDA(cudaMemcpyAsync(&next, w.totals + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
-            VPL_CUDA(cudaStreamSynchronize(s));
-            base += nF;
-            nF = next;
-            int* t = Fc; Fc = Fn; Fn = t;
+        // wide nodes for the packet traversals, breadth-first from the root
+        for (int fmt = 0; fmt < 2; ++fmt) {
+            float4* wide = (float4*)((char*)d_bvh + (fmt == 0 ? bh.off_wide : bh.off_wide4));
+            int zero = 0;
+            VPL_CUDA(cudaMemcpyAsync(w.F0, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+            int nF = 1, base = 0, levels = 0;
+            int *Fc = w.F0, *Fn = w.F1;
+            while (nF > 0) {
+                ++levels;
+                if (fmt == 0) k_wide_expand<kWide><<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.child, w.nbox, w.collapsed,
+                                                                              w.wexp, w.nint);
+                else k_wide_expand<kWide4><<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.child, w.nbox, w.collapsed,
+                                                                         w.wexp, w.nint);
+                VPL_LAUNCHED("k_wide_expand");
+                cb = w.cub_bytes;
+                VPL_CUDA(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.nint, w.noff, nF, s));
+                if (fmt == 0) k_wide_write<<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.wexp, w.nint, w.noff, base, base + nF,
+                                                                       w.nbox, w.lbox, w.collapsed, w.cnt, w.off, n,
+                                                                       Fn, wide, w.totals + 3);
+                else k_wide4_write<<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.wexp, w.nint, w.noff, base, base + nF,
+                                                                  w.nbox, w.lbox, w.collapsed, w.cnt, w.off, n, Fn,
+                                                                  wide, w.totals + 3);
+                VPL_LAUNCHED("k_wide_write");
+                int next = 0;
+                VPL_CUDA(cudaMemcpyAsync(&next, w.totals + 3, sizeof(int), cudaMemcpyDeviceToHost, s));
+                VPL_CUDA(cudaStreamSynchronize(s));
+                base += nF;
+                nF = next;
+                int* t = Fc; Fc = Fn; Fn = t;
+            }
+            int per_level = fmt == 0 ? kWide - 1 : kWide4 - 1;
+            if (per_level * levels > kWarpStack) {
+                set_error("vpl_build_bvh: %d wide levels exceed the packet stack (%d)", levels, kWarpStack);
+                return VPL_ECUDA;
+            }
         }
     }
     k_emit_tris<<<nblk(n, 256), 256, 0, s>>>(sv.verts, w.idx2, n, w.off, tris);

@@ -8,6 +8,7 @@
 #pragma once
 #include <cstdint>
 #include <cstddef>
+#include <climits>
 #include <cuda_runtime.h>
 
 #include "../../include/vplgi.h"
@@ -84,22 +85,29 @@ inline SceneView scene_view(const void* blob, int64_t n) {
 
 // BVH blob = BvhHdr, internal nodes (4 float4 each), leaf-ordered triangles
 // (3 float4 each: v0 | orig index bits, e1, e2).
-// kWide-wide node (packet traversal): SoA child boxes as centre / half extent
-// c.x[W] e.x[W] c.y[W] e.y[W] c.z[W] e.z[W], child refs[W], meta (axis,
-// n_children); children sorted by centre along `axis`, empty slots last.
-constexpr int kWide = 4;
-constexpr int kWideF4 = (6 * kWide + kWide) / 4 + 1;  // float4s per wide node (8 for W = 4)
+// Two wide node formats built from the binary PLOC tree:
+//  * 4-wide (per-ray packet traversal): SoA child boxes as centre / half
+//    extent c.x[4] e.x[4] c.y[4] e.y[4] c.z[4] e.z[4], refs[4], meta (axis,
+//    valid-slot mask) — 8 float4;
+//  * 16-wide (cone traversal, one child per lane): child c = 2 float4
+//    (lo.xyz | ref bits, hi.xyz | split-axis bits), empty slots ref INT_MIN.
+// Children are sorted by centre along the node's largest axis.
+constexpr int kWide4 = 4;
+constexpr int kWide4F4 = 8;
+constexpr int kWide = 16;
+constexpr int kWideF4 = 2 * kWide;  // float4s per 16-wide node (512 B)
 
 struct BvhHdr {
     int64_t n;
     int32_t root;       // 0 (internal) or ~0 (single leaf)
     int32_t pad;
-    int64_t off_nodes, off_tris, off_wide;
+    int64_t off_nodes, off_tris, off_wide, off_wide4;
 };
 struct BvhView {
     const float4* nodes;   // binary nodes (per-thread traversals)
     const float4* tris;
-    const float4* wide;    // kWide-wide nodes (packet traversal)
+    const float4* wide;    // 16-wide nodes (cone traversal)
+    const float4* wide4;   // 4-wide nodes (per-ray packet traversal)
     int32_t root;
 };
 inline size_t bvh_layout(int64_t n, BvhHdr* h) {
@@ -108,7 +116,11 @@ inline size_t bvh_layout(int64_t n, BvhHdr* h) {
     size_t o_n = off; off = align_up(off + sizeof(float4) * 4 * ni);
     size_t o_t = off; off = align_up(off + sizeof(float4) * 3 * (size_t)n);
     size_t o_w = off; off = align_up(off + sizeof(float4) * kWideF4 * ni);
-    if (h) { h->n = n; h->root = n > 1 ? 0 : ~0; h->off_nodes = o_n; h->off_tris = o_t; h->off_wide = o_w; }
+    size_t o_w4 = off; off = align_up(off + sizeof(float4) * kWide4F4 * ni);
+    if (h) {
+        h->n = n; h->root = n > 1 ? 0 : ~0;
+        h->off_nodes = o_n; h->off_tris = o_t; h->off_wide = o_w; h->off_wide4 = o_w4;
+    }
     return off;
 }
 inline BvhView bvh_view(const void* blob, int64_t n) {
@@ -118,6 +130,7 @@ inline BvhView bvh_view(const void* blob, int64_t n) {
     v.nodes = (const float4*)((const char*)blob + h.off_nodes);
     v.tris = (const float4*)((const char*)blob + h.off_tris);
     v.wide = (const float4*)((const char*)blob + h.off_wide);
+    v.wide4 = (const float4*)((const char*)blob + h.off_wide4);
     v.root = h.root;
     return v;
 }
@@ -239,6 +252,7 @@ __device__ __forceinline__ bool mt_hit(f3 o, f3 d, float4 a, float4 b, float4 c,
 struct TravStats {
     uint32_t boxes = 0, tris = 0;
     uint32_t wrays = 0, wsteps = 0;  // warp-level packets / iterations (counted on lane 0)
+    uint32_t aux[4] = {0, 0, 0, 0};
 };
 
 // leaf refs: ~((first << 3) | (count - 1)), count in [1, 8]
@@ -249,7 +263,7 @@ __device__ __forceinline__ void leaf_range(int node, int& first, int& count) {
 }
 
 constexpr int kStack = 128;  // > max tree depth, checked at build time (vpl_build_bvh)
-constexpr int kWarpStack = 3 * kStack;  // wide traversal pushes up to kWide-1 per level
+constexpr int kWarpStack = 512;  // >= (kWide - 1) * wide levels, checked at build time (vpl_build_bvh)
 
 // Any hit in (tmin, tmax), one ray per thread.
 template <bool kCount>
@@ -353,6 +367,87 @@ __device__ __forceinline__ bool segment_occluded(const BvhView& bv, f3 a, f3 b, 
     return bvh_any_hit<kCount>(bv, r, st);
 }
 
+struct OccluderCache {
+    int own0 = -1, own1 = -1;  // this lane's two most recent occluders (leaf-order triangle index)
+    int warp = -1;             // the warp's most recent occluder (uniform)
+    __device__ __forceinline__ void found(int tri) {
+        if (tri != own0) { own1 = own0; own0 = tri; }
+    }
+};
+
+// The packet as a cone: every live lane's shadow segment runs from its
+// receiver x_j to the common VPL position y, i.e. y + s * D_j, s in [0, 1],
+// D_j = x_j - y.  With D in the box [Dmin, Dmax], 1/D_a lies in [ilo_a, ihi_a]
+// (= [1/Dmax, 1/Dmin], or (-inf, inf) when D_a changes sign in the packet), so
+// the s-range where a segment can be inside the slab [lo_a, hi_a] is within
+// the hull of the four products (p - y_a) * {ilo_a, ihi_a}, p in {lo_a, hi_a}.
+// A box is culled only if these per-axis ranges and [0, 1] do not meet — no
+// ray of the packet can then enter it (interval arithmetic, conservative; the
+// box padding absorbs the fp32 rounding of the products).
+struct Cone {
+    f3 y, ilo, ihi;
+};
+
+__device__ __forceinline__ int fkey(float f) {   // order-preserving float -> int
+    int i = __float_as_int(f);
+    return i ^ ((i >> 31) & 0x7FFFFFFF);
+}
+__device__ __forceinline__ float fkey_inv(int k) { return __int_as_float(k ^ ((k >> 31) & 0x7FFFFFFF)); }
+
+__device__ __forceinline__ void cone_axis(float dmin, float dmax, float& ilo, float& ihi) {
+    const float inf = __int_as_float(0x7f800000);
+    bool same = dmin > 0.0f || dmax < 0.0f;
+    ilo = same ? 1.0f / dmax : -inf;
+    ihi = same ? 1.0f / dmin : inf;
+}
+
+constexpr float kConeSpread = 0.1f;  // cone traversal iff max_a (Dmax_a - Dmin_a) < kConeSpread * |D|_min
+
+__device__ __forceinline__ Cone make_cone(f3 y, f3 x, bool live, bool& tight) {
+    f3 D = x - y;
+    const int big = 0x7FFFFFFF, small = (int)0x80000000;
+    int nx = __reduce_min_sync(0xFFFFFFFFu, live ? fkey(D.x) : big);
+    int ny = __reduce_min_sync(0xFFFFFFFFu, live ? fkey(D.y) : big);
+    int nz = __reduce_min_sync(0xFFFFFFFFu, live ? fkey(D.z) : big);
+    int mx = __reduce_max_sync(0xFFFFFFFFu, live ? fkey(D.x) : small);
+    int my = __reduce_max_sync(0xFFFFFFFFu, live ? fkey(D.y) : small);
+    int mz = __reduce_max_sync(0xFFFFFFFFu, live ? fkey(D.z) : small);
+    Cone c;
+    c.y = y;
+    float dnx = fkey_inv(nx), dny = fkey_inv(ny), dnz = fkey_inv(nz);
+    float dmx = fkey_inv(mx), dmy = fkey_inv(my), dmz = fkey_inv(mz);
+    float spread = fmax3(dmx - dnx, dmy - dny, dmz - dnz);
+    // |D| of the leader lane bounds the lengths up to the spread
+    float l2 = dot(D, D);
+    float lmin = sqrtf(__int_as_float(__reduce_min_sync(0xFFFFFFFFu, live ? __float_as_int(l2) : 0x7F800000)));
+    bool straddle = !(dnx > 0.0f || dmx < 0.0f) || !(dny > 0.0f || dmy < 0.0f) || !(dnz > 0.0f || dmz < 0.0f);
+    tight = !straddle && spread < kConeSpread * lmin;
+    cone_axis(fkey_inv(nx), fkey_inv(mx), c.ilo.x, c.ihi.x);
+    cone_axis(fkey_inv(ny), fkey_inv(my), c.ilo.y, c.ihi.y);
+    cone_axis(fkey_inv(nz), fkey_inv(mz), c.ilo.z, c.ihi.z);
+    return c;
+}
+
+__device__ __forceinline__ void cone_slab(float lo, float hi, float y, float ilo, float ihi, float& s0, float& s1) {
+    float pl = lo - y, ph = hi - y;
+    float a = pl * ilo, b = pl * ihi, c = ph * ilo, d = ph * ihi;
+    s0 = fminf(fmin3(a, b, c), d);
+    s1 = fmaxf(fmax3(a, b, c), d);
+}
+
+__device__ __forceinline__ bool cone_box(const Cone& k, float4 lo, float4 hi) {
+    float x0, x1, y0, y1, z0, z1;
+    cone_slab(lo.x, hi.x, k.y.x, k.ilo.x, k.ihi.x, x0, x1);
+    cone_slab(lo.y, hi.y, k.y.y, k.ilo.y, k.ihi.y, y0, y1);
+    cone_slab(lo.z, hi.z, k.y.z, k.ilo.z, k.ihi.z, z0, z1);
+    float sn = fmax3(x0, y0, fmaxf(z0, 0.0f));
+    float sf = fmin3(x1, y1, fminf(z1, 1.0f));
+    return sn <= sf;
+}
+
+// Per-ray packet traversal of the 4-wide BVH: every live lane tests its own
+// ray against the 4 children; a child is entered if any lane's ray enters it.
+
 // Packet slab test on a wide-node child in centre / half-extent form:
 // t = (c - o) * idir -+ e * |idir| per axis — 12 FMA-pipe ops and 5 ALU ops,
 // independent of the ray's direction signs (no per-axis min/max).
@@ -366,16 +461,9 @@ __device__ __forceinline__ bool slab_ce(const Ray& r, f3 aidir, float cx, float 
     return tn <= tf;
 }
 
-struct OccluderCache {
-    int own0 = -1, own1 = -1;  // this lane's two most recent occluders (leaf-order triangle index)
-    int warp = -1;             // the warp's most recent occluder (uniform)
-    __device__ __forceinline__ void found(int tri) {
-        if (tri != own0) { own1 = own0; own0 = tri; }
-    }
-};
 
 template <bool kCount>
-__device__ __forceinline__ bool warp_traverse(const BvhView& bv, const Ray& r, bool live, bool occl,
+__device__ __forceinline__ bool warp_traverse_ray(const BvhView& bv, const Ray& r, bool live, bool occl,
                                               OccluderCache& cache, unsigned dir_neg, int* __restrict__ sstack,
                                               TravStats* st) {
     const f3 aidir = mk3(fabsf(r.idir.x), fabsf(r.idir.y), fabsf(r.idir.z));
@@ -385,7 +473,7 @@ __device__ __forceinline__ bool warp_traverse(const BvhView& bv, const Ray& r, b
         const bool go = live && !occl;
         if (kCount && (threadIdx.x & 31) == 0) st->wsteps += 1;
         if (node >= 0) {
-            const float4* nd = bv.wide + kWideF4 * node;
+            const float4* nd = bv.wide4 + kWide4F4 * node;
             float4 cx = __ldg(nd + 0), ex = __ldg(nd + 1), cy = __ldg(nd + 2), ey = __ldg(nd + 3);
             float4 cz = __ldg(nd + 4), ez = __ldg(nd + 5), rf = __ldg(nd + 6), mt = __ldg(nd + 7);
             bool h0 = slab_ce(r, aidir, cx.x, ex.x, cy.x, ey.x, cz.x, ez.x) & go;
@@ -432,17 +520,58 @@ __device__ __forceinline__ bool warp_traverse(const BvhView& bv, const Ray& r, b
     return occl;
 }
 
-// Warp-cooperative any-hit (packet traversal): the 32 lanes carry their own
-// rays but walk ONE node sequence — a child is entered if any live lane's ray
-// enters its box — so node and triangle fetches are warp-uniform broadcasts
-// and the traversal stack is warp-uniform (shared memory, one slot per level).
-// A lane may test triangles its own boxes would have culled; that cannot
-// change an any-hit result, so each lane's answer equals bvh_any_hit's.
-// Children are visited in the order of the node's split axis and the packet
-// leader's direction sign.
-// `cache` (in/out, per lane): leaf-order index of the last occluder found; it
-// is tested first (exact MT), which resolves coherent occluded rays without a
-// traversal.  Must be called by all 32 lanes with the same sstack.
+// Cone traversal of the kWide-wide BVH: lane c tests child c of the current
+// node against the packet cone; hit children are pushed onto the warp-uniform
+// shared-memory stack (first in visiting order on top).  Leaves: every live
+// lane runs the exact MT test of its own ray (O9).  Must be called by all 32
+// lanes.  A lane may test triangles its own ray would have culled; that
+// cannot change an any-hit result, so each lane's answer equals bvh_any_hit's.
+template <bool kCount>
+__device__ __forceinline__ bool warp_traverse_cone(const BvhView& bv, const Ray& r, bool live, bool occl,
+                                              OccluderCache& cache, const Cone& cone, unsigned dir_neg,
+                                              int* __restrict__ sstack, TravStats* st) {
+    const int lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
+    int sp = 0;
+    int node = bv.root;
+    while (true) {
+        if (kCount && lane == 0) st->wsteps += 1;
+        if (node >= 0) {
+            const float4* nd = bv.wide + (int64_t)kWideF4 * node + 2 * (lane & (kWide - 1));
+            float4 lo = __ldg(nd), hi = __ldg(nd + 1);
+            int ref = __float_as_int(lo.w);
+            bool hit = lane < kWide && ref != INT_MIN && cone_box(cone, lo, hi);
+            if (kCount && lane == 0) st->boxes += kWide;
+            unsigned B = __ballot_sync(0xFFFFFFFFu, hit);
+            if (B) {
+                int nh = __popc(B);
+                int rank = __popc(B & below);
+                bool rev = (dir_neg >> __float_as_int(hi.w)) & 1u;   // packet travels -axis: visit descending
+                int pos = rev ? rank : nh - 1 - rank;                 // the first to visit ends on top
+                if (hit) sstack[sp + pos] = ref;
+                sp += nh;
+                __syncwarp();
+            }
+        } else {
+            const bool go = live && !occl;
+            int first, count;
+            leaf_range(node, first, count);
+            for (int k = 0; k < count; ++k) {
+                const float4* tr = bv.tris + 3 * (first + k);
+                float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
+                float t;
+                bool hitt = mt_hit(r.o, r.d, a, b, c, r.tmin, r.tmax, t) & go & !occl;
+                if (kCount && go && !occl) st->tris += 1;
+                if (hitt) { occl = true; cache.found(first + k); }
+            }
+            if (!__any_sync(0xFFFFFFFFu, live && !occl)) break;
+        }
+        if (sp == 0) break;
+        node = sstack[--sp];
+    }
+    return occl;
+}
+
 template <bool kCount>
 __device__ __forceinline__ bool cached_occluder(const BvhView& bv, const Ray& r, int tri, TravStats* st) {
     const float4* tr = bv.tris + 3 * tri;
@@ -451,11 +580,13 @@ __device__ __forceinline__ bool cached_occluder(const BvhView& bv, const Ray& r,
     return mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t);
 }
 
+// Warp-cooperative any-hit for a packet of shadow segments x_j -> y sharing
+// the end point y (one VPL, 32 receivers).  First the exact MT tests of
+// recently found occluders (consecutive VPLs are spatially coherent: Morton
+// order), then the cone traversal for the lanes still unresolved.
 template <bool kCount>
-__device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, bool live, OccluderCache& cache,
+__device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, f3 y, bool live, OccluderCache& cache,
                                              int* __restrict__ sstack, TravStats* st) {
-    // exact MT tests of recently found occluders resolve coherent occluded rays
-    // without a traversal (consecutive VPLs are spatially coherent: Morton order)
     bool occl = false;
     if (live && cache.own0 >= 0) occl = cached_occluder<kCount>(bv, r, cache.own0, st);
     if (live && !occl && cache.own1 >= 0) occl = cached_occluder<kCount>(bv, r, cache.own1, st);
@@ -463,14 +594,25 @@ __device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, bo
         occl = cached_occluder<kCount>(bv, r, cache.warp, st);
         if (occl) cache.found(cache.warp);
     }
-    unsigned need = __ballot_sync(0xFFFFFFFFu, live && !occl);
+    bool need_lane = live && !occl;
+    bool cone_tight;
+    unsigned need = __ballot_sync(0xFFFFFFFFu, need_lane);
     if (!need) return occl;
     int leader = __ffs(need) - 1;
     unsigned neg = (r.d.x < 0.0f ? 1u : 0u) | (r.d.y < 0.0f ? 2u : 0u) | (r.d.z < 0.0f ? 4u : 0u);
     const unsigned dir_neg = __shfl_sync(0xFFFFFFFFu, neg, leader);
     if (kCount && (threadIdx.x & 31) == 0) st->wrays += 1;
+    Cone cone = make_cone(y, r.o, need_lane, cone_tight);
     bool was = occl;
-    occl = warp_traverse<kCount>(bv, r, live, occl, cache, dir_neg, sstack, st);
+    uint32_t s0 = kCount ? st->wsteps : 0;
+    if (cone_tight)
+        occl = warp_traverse_cone<kCount>(bv, r, live, occl, cache, cone, dir_neg, sstack, st);
+    else
+        occl = warp_traverse_ray<kCount>(bv, r, live, occl, cache, dir_neg, sstack, st);
+    if (kCount && (threadIdx.x & 31) == 0) {
+        st->aux[cone_tight ? 0 : 1] += 1;
+        st->aux[cone_tight ? 2 : 3] += st->wsteps - s0;
+    }
     // share the newest occluder found in this traversal with the whole warp
     unsigned fresh = __ballot_sync(0xFFFFFFFFu, occl && !was);
     if (fresh) cache.warp = __shfl_sync(0xFFFFFFFFu, cache.own0, __ffs(fresh) - 1);

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(128, 8) k_gather(SceneView sv, BvhView bv, Til
                     if (!__any_sync(0xFFFFFFFFu, traced)) continue;       // warp-uniform skip
                     Ray ray;
                     bool live = traced && segment_ray(x, v.y, eps, ray);
-                    bool occl = warp_any_hit<kCount>(bv, ray, live, cache, sstack, &st);
+                    bool occl = warp_any_hit<kCount>(bv, ray, v.y, live, cache, sstack, &st);
                     if (kCount && traced) ++n_traced;
                     if (!traced || occl) continue;
                     if (kCount) ++n_vis;
@@ -157,6 +157,11 @@ __global__ void __launch_bounds__(128, 8) k_gather(SceneView sv, BvhView bv, Til
                 atomicAdd(&ctr->warp_rays, wr);
                 atomicAdd(&ctr->warp_steps, ws);
             }
+            for (int q = 0; q < 4; ++q) {
+                unsigned long long a = st.aux[q];
+                for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+                if (lane == 0) atomicAdd(&ctr->aux[q], a);
+            }
         }
     }
 }
@@ -192,7 +197,7 @@ __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict
             if (!__any_sync(0xFFFFFFFFu, traced)) continue;
             Ray ray;
             bool live = traced && segment_ray(x, v.y, eps, ray);
-            bool occl = warp_any_hit<false>(bv, ray, live, cache, sstack, nullptr);
+            bool occl = warp_any_hit<false>(bv, ray, v.y, live, cache, sstack, nullptr);
             if (traced) tb |= 1u << b;
             if (traced && !occl) vb |= 1u << b;
         }
