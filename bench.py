@@ -94,13 +94,17 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- algorithmic op counts
-# SURVEY §8(d) per-unit figures (FP32/ALU/MUFU thread-ops), restated in DESIGN.md §5
-OPS_PAIR, OPS_TRACED, OPS_BOX, OPS_TRI = 14, 20, 17, 35
+# Per-unit thread-op counts (FMA + ALU + MUFU pipe instructions per unit of
+# algorithmic work, restated and extended in DESIGN.md §5)
+OPS = {"pairs": 14,        # d = y - x, r^2, two dots, cosine cull, self test
+       "traced": 20,       # segment setup (sqrt, 3 div), geometry term, 3 FMA accumulate
+       "box_tests": 17,    # per-ray slab test, centre/half-extent form (12 FMA-pipe + 5 ALU)
+       "cone_tests": 35,   # packet-cone x box interval test (18 FMA-pipe + 17 ALU)
+       "tri_tests": 35}    # exact Moller-Trumbore (27 FMA-pipe + 7 ALU + 1 MUFU)
 
 
-def algorithmic_ops(ctr):
-    pairs, traced, visible, boxes, tris = (int(x) for x in ctr[:5])
-    return pairs * OPS_PAIR + traced * OPS_TRACED + boxes * OPS_BOX + tris * OPS_TRI
+def algorithmic_ops(c: dict) -> int:
+    return sum(c[k] * v for k, v in OPS.items())
 
 
 # ---------------------------------------------------------------------------- our arm
@@ -179,7 +183,7 @@ def run_ours(args):
     ctr = r.ctr.clone()
     if world > 1:
         dist.all_reduce(ctr)
-    ctr = ctr.cpu().numpy()
+    ctr = V.counters_dict(ctr.cpu())
     n_hit = hit_pixels()
     M = int(r.vpls.shape[0])
     pairs_per_step = n_hit * M
@@ -249,7 +253,8 @@ def run_ours(args):
         peak_ops = sm_count * 128 * f_max                      # 4 SMSP x 32 lanes issue per clock
         ops = algorithmic_ops(ctr) / max(world, 1)              # per launch (one rank's share)
         achieved = ops / (t_gather * 1e-3)
-        pairs, traced, visible, boxes, tris, wrays, wsteps = (int(x) for x in ctr[:7])
+        c = ctr
+        pairs, traced = c["pairs"], c["traced"]
         out = {
             "metric": METRIC, "value": pairs_per_step / (t_step * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
@@ -262,11 +267,10 @@ def run_ours(args):
             "gather_ms": t_gather, "gather_pairs_per_s": pairs_per_step / (t_gather * 1e-3),
             "traced_fraction": traced / max(pairs, 1),
             "traced_pairs_per_s": traced / (t_gather * 1e-3),
-            "counters": {"pairs": pairs, "traced": traced, "visible": visible, "box_tests": boxes,
-                         "tri_tests": tris, "box_tests_per_traced": boxes / max(traced, 1),
-                         "tri_tests_per_traced": tris / max(traced, 1), "warp_rays": wrays,
-                         "warp_steps": wsteps, "lanes_per_warp_ray": traced / max(wrays, 1),
-                         "steps_per_warp_ray": wsteps / max(wrays, 1)},
+            "counters": dict(c, tri_tests_per_traced=c["tri_tests"] / max(traced, 1),
+                             steps_per_packet=c["warp_steps"] / max(c["warp_rays"], 1),
+                             cone_packet_fraction=c["cone_packets"] / max(c["warp_rays"], 1),
+                             cache_hit_fraction=c["cache_hits"] / max(traced, 1)),
             "roofline": {"bound": "alu", "kernel": "k_gather", "achieved": achieved / 1e12,
                          "peak": peak_ops / 1e12, "unit": "Tops/s", "frac": achieved / peak_ops,
                          "traffic": None,

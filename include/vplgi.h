@@ -113,16 +113,20 @@ typedef struct {
     int64_t n_near, n_lit, K, M_far, n_walks, flags, n_far_tris, n_out;
 } vpl_gen_info;
 
-/* gather counters (nullable output of vpl_gather_indirect) */
+/* gather counters (nullable output of vpl_gather_indirect; DESIGN.md §5
+ * turns them into algorithmic op counts for the roofline) */
 typedef struct {
-    unsigned long long pairs;      /* front-hit pixels x VPLs considered */
-    unsigned long long traced;     /* pairs that passed the cosine test and got a shadow ray */
-    unsigned long long visible;    /* traced pairs found unoccluded */
-    unsigned long long box_tests;  /* child-box slab tests */
-    unsigned long long tri_tests;  /* Moller-Trumbore tests */
-    unsigned long long warp_rays;  /* warp-level shadow-ray packets (>= 1 traced lane) */
-    unsigned long long warp_steps; /* warp-level traversal iterations (node or leaf visits) */
-    unsigned long long aux[4];     /* diagnostics (packet classes) */
+    unsigned long long pairs;        /* front-hit pixels x VPLs considered (Eq. 1 terms) */
+    unsigned long long traced;       /* pairs that passed the cosine test and got a shadow ray */
+    unsigned long long visible;      /* traced pairs found unoccluded */
+    unsigned long long box_tests;    /* per-ray slab tests (ray x child box, 4-wide nodes) */
+    unsigned long long tri_tests;    /* exact Moller-Trumbore tests (ray x triangle) */
+    unsigned long long warp_rays;    /* packets that needed a traversal (>= 1 unresolved lane) */
+    unsigned long long warp_steps;   /* warp-level traversal iterations (node or leaf visits) */
+    unsigned long long cone_tests;   /* packet-cone x child box tests (16-wide nodes) */
+    unsigned long long cone_packets; /* packets traversed with the cone test */
+    unsigned long long ray_packets;  /* packets traversed with per-ray tests (loose cones) */
+    unsigned long long cache_hits;   /* traced lanes resolved by the occluder cache */
 } vpl_counters;
 
 /* -------------------------------------------------------------------- */

@@ -82,6 +82,8 @@ def lib():
             "oracle_gbuffer": (None, [P, P, I64, P]),
             "oracle_gather": (None, [P, P, I64, P, I64, P, P, P, P, P]),
             "oracle_pair_visibility": (None, [P, P, P, I64, P]),
+            "oracle_near_strata": (I64, [P, P, P, I64, I64, I64, P]),
+            "oracle_walk_range": (None, [P, P, P, I64, I64, P, P]),
             "oracle_abi": (C.c_int, []),
             "oracle_threads": (C.c_int, []),
         }
@@ -232,6 +234,30 @@ class OracleScene:
         if n < 0:
             raise RuntimeError("oracle_generate_vpls: output capacity too small")
         return out[:n].copy(), info.as_dict()
+
+    def _params(self, **kw):
+        s = self.scene
+        return OParams(M=kw.get("M", s.M), K_near=kw.get("K_near", s.K_near),
+                       max_depth=kw.get("max_depth", s.max_depth), rr=kw.get("rr", s.rr),
+                       n_walks_fixed=kw.get("n_walks_fixed", 0), seed=kw.get("seed", s.seed))
+
+    def near_strata(self, labels, K, k0, k1, **kw):
+        """near VPLs of strata k0..k1-1 (K = final near count, info['K'])"""
+        p = self._params(**kw)
+        out = np.zeros(max(k1 - k0, 0), VPL_DTYPE)
+        labels = np.ascontiguousarray(labels, np.uint8)
+        lib().oracle_near_strata(self.h, _p(labels), C.byref(p), K, k0, k1, _p(out))
+        return out
+
+    def walk_range(self, labels, w0, w1, **kw):
+        """raw deposits of walks w0..w1-1 in (w, d) order (flux not divided by the walk count)"""
+        p = self._params(**kw)
+        md = max(p.max_depth, 1)
+        dep = np.zeros((w1 - w0) * md, VPL_DTYPE)
+        cnt = np.zeros(w1 - w0, np.int32)
+        labels = np.ascontiguousarray(labels, np.uint8)
+        lib().oracle_walk_range(self.h, _p(labels), C.byref(p), w0, w1, _p(dep), _p(cnt))
+        return np.concatenate([dep[i * md:i * md + c] for i, c in enumerate(cnt)]) if len(cnt) else dep[:0]
 
     # ---- O12 ----
     def gbuffer(self, pixels):

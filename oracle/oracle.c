@@ -732,6 +732,32 @@ void oracle_pair_visibility(const OScene* s, const float* x, const float* y, int
     for (int64_t i = 0; i < n; i++) vis[i] = (uint8_t)!occluded(s, ld3(x + 3 * i), ld3(y + 3 * i));
 }
 
+/* Sampled full-size checks: strata k0..k1-1 of the near part (same table as
+ * oracle_generate_vpls builds; K = the final near count) and the raw
+ * deposits of walks w0..w1-1 (flux not yet divided by the walk count). */
+int64_t oracle_near_strata(const OScene* s, const uint8_t* labels, const OParams* p, int64_t K, int64_t k0, int64_t k1,
+                           OVpl* out) {
+    uint8_t* lit = (uint8_t*)malloc(s->n);
+    int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (s->n + 1));
+    uint64_t* P = (uint64_t*)malloc(sizeof(uint64_t) * (s->n + 1));
+    oracle_lit(s, labels, lit);
+    int64_t m = oracle_near_table(s, lit, order, P, NULL);
+    if (m > 0 && K > 0) {
+        float D = (float)((double)P[m - 1] / (double)K / 1099511627776.0);
+#pragma omp parallel for schedule(dynamic, 8)
+        for (int64_t k = k0; k < k1; k++) near_vpl(s, p, order, P, m, K, D, k, out + (k - k0));
+    }
+    free(lit); free(order); free(P);
+    return m;
+}
+
+void oracle_walk_range(const OScene* s, const uint8_t* labels, const OParams* p, int64_t w0, int64_t w1, OVpl* dep,
+                       int32_t* cnt) {
+    int64_t md = p->max_depth > 0 ? p->max_depth : 1;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t w = w0; w < w1; w++) cnt[w - w0] = walk(s, p, labels, (uint32_t)w, dep + (w - w0) * md);
+}
+
 int oracle_abi(void) { return ORACLE_ABI; }
 int oracle_threads(void) {
 #ifdef _OPENMP

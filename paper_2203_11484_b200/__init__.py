@@ -50,10 +50,18 @@ class vpl_gen_info(C.Structure):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}
 
 
+COUNTER_NAMES = ["pairs", "traced", "visible", "box_tests", "tri_tests", "warp_rays", "warp_steps", "cone_tests",
+                 "cone_packets", "ray_packets", "cache_hits"]
+
+
 class vpl_counters(C.Structure):
-    _fields_ = [("pairs", C.c_uint64), ("traced", C.c_uint64), ("visible", C.c_uint64),
-                ("box_tests", C.c_uint64), ("tri_tests", C.c_uint64), ("warp_rays", C.c_uint64),
-                ("warp_steps", C.c_uint64), ("aux", C.c_uint64 * 4)]
+    _fields_ = [(k, C.c_uint64) for k in COUNTER_NAMES]
+
+
+def counters_dict(ctr) -> dict:
+    """vpl_counters tensor (int64[11]) -> {name: int}"""
+    vals = ctr.tolist() if hasattr(ctr, "tolist") else list(ctr)
+    return {k: int(v) for k, v in zip(COUNTER_NAMES, vals)}
 
 
 VPL_RECORD_BYTES = 48
@@ -265,7 +273,7 @@ def gather_indirect(scene, bvh, gbuf, vpls, tiles, W, H, tw=16, th=16, rgb=None,
     wb = C.c_size_t()
     _check(load_library().vpl_gather_bytes(C.byref(wb)), "vpl_gather_bytes")
     work = work if work is not None else torch.empty(wb.value, dtype=torch.uint8, device=dev)
-    ctr = torch.zeros(11, dtype=torch.int64, device=dev) if counters else None
+    ctr = torch.zeros(len(COUNTER_NAMES), dtype=torch.int64, device=dev) if counters else None
     nv = vpls.shape[0] if vpls.dim() == 2 else vpls.numel() // VPL_RECORD_BYTES
     _check(load_library().vpl_gather_indirect(_ptr(scene), _ptr(bvh), _ptr(gbuf), _ptr(vpls), nv, _ptr(tiles),
                                               tiles.numel(), tw, th, _ptr(rgb), _ptr(ctr), _ptr(work), work.numel(),

@@ -252,7 +252,7 @@ __device__ __forceinline__ bool mt_hit(f3 o, f3 d, float4 a, float4 b, float4 c,
 struct TravStats {
     uint32_t boxes = 0, tris = 0;
     uint32_t wrays = 0, wsteps = 0;  // warp-level packets / iterations (counted on lane 0)
-    uint32_t aux[4] = {0, 0, 0, 0};
+    uint32_t cones = 0, cpk = 0, rpk = 0, chits = 0;  // cone tests, cone / per-ray packets, cache hits
 };
 
 // leaf refs: ~((first << 3) | (count - 1)), count in [1, 8]
@@ -541,7 +541,7 @@ __device__ __forceinline__ bool warp_traverse_cone(const BvhView& bv, const Ray&
             float4 lo = __ldg(nd), hi = __ldg(nd + 1);
             int ref = __float_as_int(lo.w);
             bool hit = lane < kWide && ref != INT_MIN && cone_box(cone, lo, hi);
-            if (kCount && lane == 0) st->boxes += kWide;
+            if (kCount && lane == 0) st->cones += kWide;
             unsigned B = __ballot_sync(0xFFFFFFFFu, hit);
             if (B) {
                 int nh = __popc(B);
@@ -595,6 +595,7 @@ __device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, f3
         if (occl) cache.found(cache.warp);
     }
     bool need_lane = live && !occl;
+    if (kCount && live && occl) st->chits += 1;
     bool cone_tight;
     unsigned need = __ballot_sync(0xFFFFFFFFu, need_lane);
     if (!need) return occl;
@@ -604,14 +605,12 @@ __device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, f3
     if (kCount && (threadIdx.x & 31) == 0) st->wrays += 1;
     Cone cone = make_cone(y, r.o, need_lane, cone_tight);
     bool was = occl;
-    uint32_t s0 = kCount ? st->wsteps : 0;
     if (cone_tight)
         occl = warp_traverse_cone<kCount>(bv, r, live, occl, cache, cone, dir_neg, sstack, st);
     else
         occl = warp_traverse_ray<kCount>(bv, r, live, occl, cache, dir_neg, sstack, st);
     if (kCount && (threadIdx.x & 31) == 0) {
-        st->aux[cone_tight ? 0 : 1] += 1;
-        st->aux[cone_tight ? 2 : 3] += st->wsteps - s0;
+        if (cone_tight) st->cpk += 1; else st->rpk += 1;
     }
     // share the newest occluder found in this traversal with the whole warp
     unsigned fresh = __ballot_sync(0xFFFFFFFFu, occl && !was);

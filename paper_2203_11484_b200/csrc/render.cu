@@ -140,27 +140,13 @@ __global__ void __launch_bounds__(128, 8) k_gather(SceneView sv, BvhView bv, Til
         }
         if (kCount) {
             unsigned long long pairs = active ? (unsigned long long)M : 0ull;
-            unsigned long long bx = st.boxes, tt = st.tris, wr = st.wrays, ws = st.wsteps;
-            for (int o = 16; o > 0; o >>= 1) {
-                pairs += __shfl_xor_sync(0xFFFFFFFFu, pairs, o);
-                n_traced += __shfl_xor_sync(0xFFFFFFFFu, n_traced, o);
-                n_vis += __shfl_xor_sync(0xFFFFFFFFu, n_vis, o);
-                bx += __shfl_xor_sync(0xFFFFFFFFu, bx, o);
-                tt += __shfl_xor_sync(0xFFFFFFFFu, tt, o);
-            }
-            if (lane == 0) {
-                atomicAdd(&ctr->pairs, pairs);
-                atomicAdd(&ctr->traced, n_traced);
-                atomicAdd(&ctr->visible, n_vis);
-                atomicAdd(&ctr->box_tests, bx);
-                atomicAdd(&ctr->tri_tests, tt);
-                atomicAdd(&ctr->warp_rays, wr);
-                atomicAdd(&ctr->warp_steps, ws);
-            }
-            for (int q = 0; q < 4; ++q) {
-                unsigned long long a = st.aux[q];
+            unsigned long long v[11] = {pairs, n_traced, n_vis, st.boxes, st.tris, st.wrays, st.wsteps,
+                                        st.cones, st.cpk, st.rpk, st.chits};
+#pragma unroll
+            for (int q = 0; q < 11; ++q) {
+                unsigned long long a = v[q];
                 for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
-                if (lane == 0) atomicAdd(&ctr->aux[q], a);
+                if (lane == 0) atomicAdd(&ctr->pairs + q, a);
             }
         }
     }
