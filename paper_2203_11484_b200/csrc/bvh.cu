@@ -263,6 +263,14 @@ __global__ void k_emit_nodes(int64_t n, const int2* __restrict__ child, const fl
 
 // ---------------------------------------------------------------- kWide-wide collapse (BFS levels)
 __device__ __forceinline__ bool is_inner(int r, const uint8_t* __restrict__ collapsed) { return r >= 0 && !collapsed[r]; }
+// The 16-wide (cone) tree opens the SAH leaves too: its leaves are single
+// triangles, each with its own box tested against the packet cone in
+// parallel with its siblings, so the per-lane exact MT tests only run on
+// triangles the cone can reach.  (The 4-wide per-ray tree keeps the SAH leaves.)
+template <int kW>
+__device__ __forceinline__ bool is_inner_w(int r, const uint8_t* __restrict__ collapsed) {
+    return kW == kWide ? r >= 0 : is_inner(r, collapsed);
+}
 
 __device__ __forceinline__ void ref_box(int r, const float4* __restrict__ nbox, const float4* __restrict__ lbox,
                                         float4& lo, float4& hi) {
@@ -286,7 +294,7 @@ __global__ void k_wide_expand(const int* __restrict__ F, int nF, const int2* __r
         int best = -1;
         float ba = -1.0f;
         for (int k = 0; k < cntc; ++k)
-            if (is_inner(ref[k], collapsed)) {
+            if (is_inner_w<kW>(ref[k], collapsed)) {
                 float a = half_area(nbox[2 * ref[k]], nbox[2 * ref[k] + 1]);
                 if (a > ba) { ba = a; best = k; }
             }
@@ -299,7 +307,7 @@ __global__ void k_wide_expand(const int* __restrict__ F, int nF, const int2* __r
     for (int k = 0; k < kW; ++k) {
         int r = k < cntc ? ref[k] : INT_MIN;
         exp[f * kW + k] = r;
-        ni += (k < cntc && is_inner(r, collapsed)) ? 1 : 0;
+        ni += (k < cntc && is_inner_w<kW>(r, collapsed)) ? 1 : 0;
     }
     nint[f] = ni;
 }
@@ -347,12 +355,10 @@ __global__ void k_wide_write(const int* __restrict__ F, int nF, const int* __res
         float4 lo, hi;
         ref_box(r, nbox, lbox, lo, hi);
         int out;
-        if (is_inner(r, collapsed)) {
+        if (is_inner_w<kWide>(r, collapsed)) {
             int slot = noff[f] + j++;
             Fnext[slot] = r;
             out = base_next + slot;
-        } else if (r >= 0) {
-            out = leaf_ref(toff[r], cnt[r]);
         } else {
             out = leaf_ref(toff[(n - 1) + (~r)], 1);
         }
@@ -611,7 +617,7 @@ int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* 
                 nF = next;
                 int* t = Fc; Fc = Fn; Fn = t;
             }
-            int per_level = fmt == 0 ? kWide - 1 : kWide4 - 1;
+            int per_level = fmt == 0 ? 2 * kWide : kWide4 - 1;   // the cone traversal expands two nodes per step
             if (per_level * levels > kWarpStack) {
                 set_error("vpl_build_bvh: %d wide levels exceed the packet stack (%d)", levels, kWarpStack);
                 return VPL_ECUDA;

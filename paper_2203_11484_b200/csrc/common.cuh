@@ -263,7 +263,7 @@ __device__ __forceinline__ void leaf_range(int node, int& first, int& count) {
 }
 
 constexpr int kStack = 128;  // > max tree depth, checked at build time (vpl_build_bvh)
-constexpr int kWarpStack = 512;  // >= (kWide - 1) * wide levels, checked at build time (vpl_build_bvh)
+constexpr int kWarpStack = 512;  // >= 2 * kWide * wide levels, checked at build time (vpl_build_bvh)
 
 // Any hit in (tmin, tmax), one ray per thread.
 template <bool kCount>
@@ -349,14 +349,25 @@ __device__ __forceinline__ int bvh_closest(const BvhView& bv, const Ray& r, floa
 }
 
 // unoccluded(a, b) with the eps-shrunk segment (O9) — segment setup shared by
-// the per-thread and the warp-cooperative traversals
-__device__ __forceinline__ bool segment_ray(f3 a, f3 b, float eps, Ray& r) {
+// the per-thread and the warp-cooperative traversals.  seg_ray() leaves the
+// slab-test fields (idir, ood) unset: the warp traversal derives them only on
+// its per-ray path (with_slab()).
+__device__ __forceinline__ bool seg_ray(f3 a, f3 b, float eps, Ray& r) {
     f3 d = b - a;
     float dist = sqrtf(dot(d, d));
-    f3 dir = mk3(d.x / dist, d.y / dist, d.z / dist);
-    float tmin = eps, tmax = dist - eps;
-    if (!(tmax > tmin)) return false;
-    r = make_ray(a, dir, tmin, tmax);
+    r.o = a;
+    r.d = mk3(d.x / dist, d.y / dist, d.z / dist);
+    r.tmin = eps;
+    r.tmax = dist - eps;
+    return r.tmax > r.tmin;
+}
+__device__ __forceinline__ void with_slab(Ray& r) {
+    r.idir = mk3(1.0f / nudge(r.d.x), 1.0f / nudge(r.d.y), 1.0f / nudge(r.d.z));
+    r.ood = mk3(r.o.x * r.idir.x, r.o.y * r.idir.y, r.o.z * r.idir.z);
+}
+__device__ __forceinline__ bool segment_ray(f3 a, f3 b, float eps, Ray& r) {
+    if (!seg_ray(a, b, eps, r)) return false;
+    with_slab(r);
     return true;
 }
 
@@ -386,6 +397,7 @@ struct OccluderCache {
 // box padding absorbs the fp32 rounding of the products).
 struct Cone {
     f3 y, ilo, ihi;
+    float s_lo, s_hi;   // s-range that can hold an occluder of any packet segment (eps caps removed)
 };
 
 __device__ __forceinline__ int fkey(float f) {   // order-preserving float -> int
@@ -403,7 +415,7 @@ __device__ __forceinline__ void cone_axis(float dmin, float dmax, float& ilo, fl
 
 constexpr float kConeSpread = 0.1f;  // cone traversal iff max_a (Dmax_a - Dmin_a) < kConeSpread * |D|_min
 
-__device__ __forceinline__ Cone make_cone(f3 y, f3 x, bool live, bool& tight) {
+__device__ __forceinline__ Cone make_cone(f3 y, f3 x, bool live, float eps, bool& tight) {
     f3 D = x - y;
     const int big = 0x7FFFFFFF, small = (int)0x80000000;
     int nx = __reduce_min_sync(0xFFFFFFFFu, live ? fkey(D.x) : big);
@@ -422,6 +434,12 @@ __device__ __forceinline__ Cone make_cone(f3 y, f3 x, bool live, bool& tight) {
     float lmin = sqrtf(__int_as_float(__reduce_min_sync(0xFFFFFFFFu, live ? __float_as_int(l2) : 0x7F800000)));
     bool straddle = !(dnx > 0.0f || dmx < 0.0f) || !(dny > 0.0f || dmy < 0.0f) || !(dnz > 0.0f || dmz < 0.0f);
     tight = !straddle && spread < kConeSpread * lmin;
+    // Segment j only tests t in (eps, |D_j| - eps), i.e. s = 1 - t/|D_j| in (eps/|D_j|, 1 - eps/|D_j|),
+    // inside [eps/|D|max, 1 - eps/|D|max].  Half of that cap is cut off (the other half is slack for
+    // the rounding of the exact MT t), which culls the receiver's and the VPL's own surfaces.
+    float lmax = sqrtf(__int_as_float(__reduce_max_sync(0xFFFFFFFFu, live ? __float_as_int(l2) : 0)));
+    c.s_lo = 0.5f * eps / lmax;
+    c.s_hi = 1.0f - c.s_lo;
     cone_axis(fkey_inv(nx), fkey_inv(mx), c.ilo.x, c.ihi.x);
     cone_axis(fkey_inv(ny), fkey_inv(my), c.ilo.y, c.ihi.y);
     cone_axis(fkey_inv(nz), fkey_inv(mz), c.ilo.z, c.ihi.z);
@@ -440,8 +458,8 @@ __device__ __forceinline__ bool cone_box(const Cone& k, float4 lo, float4 hi) {
     cone_slab(lo.x, hi.x, k.y.x, k.ilo.x, k.ihi.x, x0, x1);
     cone_slab(lo.y, hi.y, k.y.y, k.ilo.y, k.ihi.y, y0, y1);
     cone_slab(lo.z, hi.z, k.y.z, k.ilo.z, k.ihi.z, z0, z1);
-    float sn = fmax3(x0, y0, fmaxf(z0, 0.0f));
-    float sf = fmin3(x1, y1, fminf(z1, 1.0f));
+    float sn = fmax3(x0, y0, fmaxf(z0, k.s_lo));
+    float sf = fmin3(x1, y1, fminf(z1, k.s_hi));
     return sn <= sf;
 }
 
@@ -463,9 +481,10 @@ __device__ __forceinline__ bool slab_ce(const Ray& r, f3 aidir, float cx, float 
 
 
 template <bool kCount>
-__device__ __forceinline__ bool warp_traverse_ray(const BvhView& bv, const Ray& r, bool live, bool occl,
+__device__ __forceinline__ bool warp_traverse_ray(const BvhView& bv, Ray r, bool live, bool occl,
                                               OccluderCache& cache, unsigned dir_neg, int* __restrict__ sstack,
                                               TravStats* st) {
+    with_slab(r);
     const f3 aidir = mk3(fabsf(r.idir.x), fabsf(r.idir.y), fabsf(r.idir.z));
     int sp = 0;
     int node = bv.root;
@@ -520,54 +539,76 @@ __device__ __forceinline__ bool warp_traverse_ray(const BvhView& bv, const Ray& 
     return occl;
 }
 
-// Cone traversal of the kWide-wide BVH: lane c tests child c of the current
-// node against the packet cone; hit children are pushed onto the warp-uniform
-// shared-memory stack (first in visiting order on top).  Leaves: every live
-// lane runs the exact MT test of its own ray (O9).  Must be called by all 32
-// lanes.  A lane may test triangles its own ray would have culled; that
-// cannot change an any-hit result, so each lane's answer equals bvh_any_hit's.
+// Cone traversal of the kWide-wide BVH (kWide = 16, leaves = single
+// triangles).  Each step pops up to two nodes: lanes 0-15 test the children of
+// the first against the packet cone, lanes 16-31 those of the second.  Hit
+// triangle children are resolved at once — every live lane runs the exact MT
+// test of its own ray (O9) — and hit inner children are pushed onto the
+// warp-uniform shared-memory stack, the first node's children on top in
+// visiting order (the order differs from a one-node-per-step depth-first
+// traversal only in that the second node is opened early).  Must be called by all 32 lanes.  A lane may test triangles its
+// own ray would have culled; that cannot change an any-hit result, so each
+// lane's answer equals bvh_any_hit's.
 template <bool kCount>
 __device__ __forceinline__ bool warp_traverse_cone(const BvhView& bv, const Ray& r, bool live, bool occl,
                                               OccluderCache& cache, const Cone& cone, unsigned dir_neg,
                                               int* __restrict__ sstack, TravStats* st) {
     const int lane = threadIdx.x & 31;
+    const int half = lane >> 4;
     const unsigned below = (1u << lane) - 1u;
+    const unsigned hmask = half ? 0xFFFF0000u : 0x0000FFFFu;
+    if (bv.root < 0) {  // single-triangle scene
+        const float4* tr = bv.tris;
+        float t;
+        bool hitt = mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t) & live & !occl;
+        if (kCount && live && !occl) st->tris += 1;
+        if (hitt) { occl = true; cache.found(0); }
+        return occl;
+    }
     int sp = 0;
-    int node = bv.root;
+    int nodeA = bv.root;
     while (true) {
+        int nodeB = -1;
+        if (sp > 0) nodeB = sstack[--sp];
         if (kCount && lane == 0) st->wsteps += 1;
+        const int node = half ? nodeB : nodeA;
+        bool hit = false;
+        int ref = INT_MIN;
+        int axis = 0;
         if (node >= 0) {
             const float4* nd = bv.wide + (int64_t)kWideF4 * node + 2 * (lane & (kWide - 1));
             float4 lo = __ldg(nd), hi = __ldg(nd + 1);
-            int ref = __float_as_int(lo.w);
-            bool hit = lane < kWide && ref != INT_MIN && cone_box(cone, lo, hi);
-            if (kCount && lane == 0) st->cones += kWide;
-            unsigned B = __ballot_sync(0xFFFFFFFFu, hit);
-            if (B) {
-                int nh = __popc(B);
-                int rank = __popc(B & below);
-                bool rev = (dir_neg >> __float_as_int(hi.w)) & 1u;   // packet travels -axis: visit descending
-                int pos = rev ? rank : nh - 1 - rank;                 // the first to visit ends on top
-                if (hit) sstack[sp + pos] = ref;
-                sp += nh;
-                __syncwarp();
-            }
-        } else {
+            ref = __float_as_int(lo.w);
+            axis = __float_as_int(hi.w);
+            hit = ref != INT_MIN && cone_box(cone, lo, hi);
+        }
+        if (kCount && lane == 0) st->cones += nodeB >= 0 ? 2 * kWide : kWide;
+        const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
+        unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
+        if (Bi) {
+            const int nB = __popc(Bi >> 16), nA = __popc(Bi & 0xFFFFu);
+            const int nh = half ? nB : nA;
+            const int rank = __popc(Bi & below & hmask);
+            const bool rev = (dir_neg >> axis) & 1u;       // packet travels -axis: visit descending
+            const int pos = (half ? 0 : nB) + (rev ? rank : nh - 1 - rank);   // first to visit ends on top
+            if (hit && ref >= 0) sstack[sp + pos] = ref;
+            sp += nA + nB;
+            __syncwarp();
+        }
+        while (Bl) {
+            const int k = __ffs(Bl) - 1;
+            Bl &= Bl - 1u;
+            const int tri = ~__shfl_sync(0xFFFFFFFFu, ref, k) >> 3;
             const bool go = live && !occl;
-            int first, count;
-            leaf_range(node, first, count);
-            for (int k = 0; k < count; ++k) {
-                const float4* tr = bv.tris + 3 * (first + k);
-                float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
-                float t;
-                bool hitt = mt_hit(r.o, r.d, a, b, c, r.tmin, r.tmax, t) & go & !occl;
-                if (kCount && go && !occl) st->tris += 1;
-                if (hitt) { occl = true; cache.found(first + k); }
-            }
-            if (!__any_sync(0xFFFFFFFFu, live && !occl)) break;
+            const float4* tr = bv.tris + 3 * tri;
+            float t;
+            bool hitt = mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t) & go;
+            if (kCount && go) st->tris += 1;
+            if (hitt) { occl = true; cache.found(tri); }
+            if (!__any_sync(0xFFFFFFFFu, live && !occl)) return occl;
         }
         if (sp == 0) break;
-        node = sstack[--sp];
+        nodeA = sstack[--sp];
     }
     return occl;
 }
@@ -585,8 +626,8 @@ __device__ __forceinline__ bool cached_occluder(const BvhView& bv, const Ray& r,
 // recently found occluders (consecutive VPLs are spatially coherent: Morton
 // order), then the cone traversal for the lanes still unresolved.
 template <bool kCount>
-__device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, f3 y, bool live, OccluderCache& cache,
-                                             int* __restrict__ sstack, TravStats* st) {
+__device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, f3 y, float eps, bool live,
+                                             OccluderCache& cache, int* __restrict__ sstack, TravStats* st) {
     bool occl = false;
     if (live && cache.own0 >= 0) occl = cached_occluder<kCount>(bv, r, cache.own0, st);
     if (live && !occl && cache.own1 >= 0) occl = cached_occluder<kCount>(bv, r, cache.own1, st);
@@ -596,6 +637,7 @@ __device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, f3
     }
     bool need_lane = live && !occl;
     if (kCount && live && occl) st->chits += 1;
+    // (the per-ray fallback derives its own slab fields)
     bool cone_tight;
     unsigned need = __ballot_sync(0xFFFFFFFFu, need_lane);
     if (!need) return occl;
@@ -603,7 +645,7 @@ __device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, f3
     unsigned neg = (r.d.x < 0.0f ? 1u : 0u) | (r.d.y < 0.0f ? 2u : 0u) | (r.d.z < 0.0f ? 4u : 0u);
     const unsigned dir_neg = __shfl_sync(0xFFFFFFFFu, neg, leader);
     if (kCount && (threadIdx.x & 31) == 0) st->wrays += 1;
-    Cone cone = make_cone(y, r.o, need_lane, cone_tight);
+    Cone cone = make_cone(y, r.o, need_lane, eps, cone_tight);
     bool was = occl;
     if (cone_tight)
         occl = warp_traverse_cone<kCount>(bv, r, live, occl, cache, cone, dir_neg, sstack, st);

@@ -116,8 +116,8 @@ __global__ void __launch_bounds__(128, 8) k_gather(SceneView sv, BvhView bv, Til
                     bool traced = active && v.tri != tri_x && cx > 0.0f && ci > 0.0f;
                     if (!__any_sync(0xFFFFFFFFu, traced)) continue;       // warp-uniform skip
                     Ray ray;
-                    bool live = traced && segment_ray(x, v.y, eps, ray);
-                    bool occl = warp_any_hit<kCount>(bv, ray, v.y, live, cache, sstack, &st);
+                    bool live = traced && seg_ray(x, v.y, eps, ray);
+                    bool occl = warp_any_hit<kCount>(bv, ray, v.y, eps, live, cache, sstack, &st);
                     if (kCount && traced) ++n_traced;
                     if (!traced || occl) continue;
                     if (kCount) ++n_vis;
@@ -182,8 +182,8 @@ __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict
             bool traced = active && v.tri != tri_x && cx > 0.0f && ci > 0.0f;
             if (!__any_sync(0xFFFFFFFFu, traced)) continue;
             Ray ray;
-            bool live = traced && segment_ray(x, v.y, eps, ray);
-            bool occl = warp_any_hit<false>(bv, ray, v.y, live, cache, sstack, nullptr);
+            bool live = traced && seg_ray(x, v.y, eps, ray);
+            bool occl = warp_any_hit<false>(bv, ray, v.y, eps, live, cache, sstack, nullptr);
             if (traced) tb |= 1u << b;
             if (traced && !occl) vb |= 1u << b;
         }
