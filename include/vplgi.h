@@ -202,8 +202,10 @@ VPL_API int32_t vpl_render_gbuffer(const void* d_scene, const void* d_bvh, const
 /* a8  gather_indirect (Eq. 1; O13): indirect-only linear radiance
  * d_rgb float[H*W*3] for the listed tiles (others untouched).  Miss or
  * back-face pixels get 0.  d_ctr (nullable) accumulates counters.
- * d_work: vpl_gather_bytes() bytes (tile queue). */
-VPL_API int32_t vpl_gather_bytes(size_t* work_bytes);
+ * d_work: vpl_gather_bytes(n_vpls) bytes (tile queue + a Morton-ordered copy
+ * of the VPLs: Eq. 1 is a sum over the set, the gather visits it in spatial
+ * order; the caller's array is not modified). */
+VPL_API int32_t vpl_gather_bytes(int32_t n_vpls, size_t* work_bytes);
 VPL_API int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf,
                             const vpl_record* d_vpls, int32_t n_vpls, const int32_t* d_tiles, int32_t n_tiles,
                             int32_t tile_w, int32_t tile_h, float* d_rgb, vpl_counters* d_ctr, void* d_work,

@@ -75,7 +75,7 @@ def load_library(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("VPLGI_LIB", LIB_PATH))   # VPLGI_LIB: tuning variants (tools/)
     if not p.exists():
         raise ImportError(f"libvplgi.so not built at {p}; run `python -c 'import __graft_entry__ as g; g.build()'`")
     L = C.CDLL(str(p))
@@ -96,7 +96,7 @@ def load_library(path: str | os.PathLike | None = None):
         "vpl_generate_bytes": (I32, [P, I64, I64, P]),
         "vpl_generate_vpls": (I32, [P, P, P, P, P, I64, P, P, SZ, P]),
         "vpl_render_gbuffer": (I32, [P, P, P, I32, I32, I32, P, P]),
-        "vpl_gather_bytes": (I32, [P]),
+        "vpl_gather_bytes": (I32, [I32, P]),
         "vpl_gather_indirect": (I32, [P, P, P, P, I32, P, I32, I32, I32, P, P, P, SZ, P]),
         "vpl_visibility_dump": (I32, [P, P, P, P, I32, P, I32, P, P, P]),
         "vpl_closest_hit_batch": (I32, [P, P, P, P, I64, F, F, P, P, P]),
@@ -270,11 +270,12 @@ def gather_indirect(scene, bvh, gbuf, vpls, tiles, W, H, tw=16, th=16, rgb=None,
                     stream=None):
     dev = scene.device
     rgb = rgb if rgb is not None else torch.zeros(H * W * 3, dtype=torch.float32, device=dev)
-    wb = C.c_size_t()
-    _check(load_library().vpl_gather_bytes(C.byref(wb)), "vpl_gather_bytes")
-    work = work if work is not None else torch.empty(wb.value, dtype=torch.uint8, device=dev)
-    ctr = torch.zeros(len(COUNTER_NAMES), dtype=torch.int64, device=dev) if counters else None
     nv = vpls.shape[0] if vpls.dim() == 2 else vpls.numel() // VPL_RECORD_BYTES
+    wb = C.c_size_t()
+    _check(load_library().vpl_gather_bytes(nv, C.byref(wb)), "vpl_gather_bytes")
+    if work is None or work.numel() < wb.value:
+        work = torch.empty(wb.value, dtype=torch.uint8, device=dev)
+    ctr = torch.zeros(len(COUNTER_NAMES), dtype=torch.int64, device=dev) if counters else None
     _check(load_library().vpl_gather_indirect(_ptr(scene), _ptr(bvh), _ptr(gbuf), _ptr(vpls), nv, _ptr(tiles),
                                               tiles.numel(), tw, th, _ptr(rgb), _ptr(ctr), _ptr(work), work.numel(),
                                               _stream(stream)), "vpl_gather_indirect")

@@ -26,28 +26,32 @@ def _headers():
     return list(CSRC.glob("*.cuh")) + list(INC.glob("*.h"))
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    OBJ.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: Path | None = None) -> Path:
+    """Build libvplgi.so; `defines`/`out` build a tuning variant (tools/ only) into its own file."""
+    lib = Path(out) if out else LIB
+    obj = OBJ if not defines else OBJ / ("v_" + "_".join(d.replace("=", "") for d in defines))
+    obj.mkdir(parents=True, exist_ok=True)
+    flags = NVCC_FLAGS + [f"-D{d}" for d in defines]
     hdr_mtime = max(p.stat().st_mtime for p in _headers())
     objs = []
     for src in SOURCES:
         s = CSRC / src
-        o = OBJ / (s.stem + ".o")
+        o = obj / (s.stem + ".o")
         objs.append(o)
         if force or not o.exists() or o.stat().st_mtime < max(s.stat().st_mtime, hdr_mtime):
-            cmd = [NVCC, *NVCC_FLAGS, "-c", str(s), "-o", str(o)]
+            cmd = [NVCC, *flags, "-c", str(s), "-o", str(o)]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             subprocess.check_call(cmd)
-    if force or not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
-        tmp = LIB.with_suffix(f".{os.getpid()}.tmp")
+    if force or not lib.exists() or lib.stat().st_mtime < max(o.stat().st_mtime for o in objs):
+        tmp = lib.with_suffix(f".{os.getpid()}.tmp")
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp), *map(str, objs),
                "-Xcompiler", "-fPIC"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

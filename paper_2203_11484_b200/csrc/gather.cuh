@@ -1,0 +1,345 @@
+// gather.cuh — the warp-cooperative shadow-ray engine of the a8 gather
+// (Eq. 1; DESIGN.md §3 O13 and §5).
+//
+// A warp owns 32 receivers x_j (one per lane).  It walks the VPL array in
+// order, in *groups* of up to kGroup consecutive VPLs whose positions lie
+// close together (consecutive near VPLs are neighbouring strata of the
+// Morton-ordered patch table).  For a group, every lane computes the
+// Eq. 1 cosine terms of its receiver against each VPL of the group (exact
+// fp32, O13), and the shadow segments x_j -> y_k that need a visibility test
+// are resolved together:
+//   1. occluder cache: exact MT tests against the lane's two latest occluders
+//      and the warp's latest one;
+//   2. beam traversal of the 16-wide BVH (leaves = single triangles): all
+//      remaining segments lie in the beam {y + s*D : y in Ybox, D in Dbox,
+//      s in [s_lo, s_hi]}; lane c of each half-warp tests child c of a node
+//      against it (interval arithmetic, two nodes per step), hit inner
+//      children go on a warp-uniform shared-memory stack, hit triangles are
+//      tested at once by every lane against each of its pending segments
+//      with the exact MT of O9 (the terms that depend only on the origin and
+//      the triangle are shared between a lane's segments — same operations,
+//      same bits);
+//   3. loose beams (a D component changes sign, or the spread of D is large)
+//      are split into single-VPL beams, and loose single beams fall back to
+//      the per-ray packet traversal of the 4-wide BVH.
+// Every lane's answer equals the exact any-hit of O9 for each of its
+// segments: the beam and the boxes are conservative (boxes padded at build
+// time), and extra MT tests cannot change an any-hit result.
+#pragma once
+#include "common.cuh"
+
+namespace vplgi {
+
+#ifndef VPL_GROUP
+#define VPL_GROUP 1
+#endif
+#ifndef VPL_GROUP_TOL
+#define VPL_GROUP_TOL 0.05f
+#endif
+constexpr int kGroup = VPL_GROUP;          // max VPLs per group
+constexpr float kGroupTol = VPL_GROUP_TOL; // group iff the VPL box extent < tol * distance to the warp's receivers
+
+// Beam: per axis a, a segment point y + s*D can lie in the slab [lo, hi] only
+// for s in [s0, s1] with (D_a > 0)  s0 = (lo - yhi)/Dmax, s1 = (hi - ylo)/Dmin
+//                        (D_a < 0)  s0 = (hi - ylo)/Dmin, s1 = (lo - yhi)/Dmax
+// (s > 0; y and D range independently over their boxes, a superset of the
+// actual segments).  Stored as s0 = N*a0 - b0, s1 = F*a1 - b1 with N/F the
+// box face picked by the sign of D_a; evaluated with one FFMA each.  The
+// rounding (position error ~ulp(coord)) is absorbed by the box padding.
+struct Beam {
+    float a0[3], b0[3], a1[3], b1[3];
+    float s_lo, s_hi;
+    unsigned pos;   // bit a: D_a > 0
+};
+
+__device__ __forceinline__ bool beam_box(const Beam& B, float4 lo, float4 hi) {
+    const bool px = B.pos & 1u, py = B.pos & 2u, pz = B.pos & 4u;
+    float s0x = fmaf(px ? lo.x : hi.x, B.a0[0], -B.b0[0]), s1x = fmaf(px ? hi.x : lo.x, B.a1[0], -B.b1[0]);
+    float s0y = fmaf(py ? lo.y : hi.y, B.a0[1], -B.b0[1]), s1y = fmaf(py ? hi.y : lo.y, B.a1[1], -B.b1[1]);
+    float s0z = fmaf(pz ? lo.z : hi.z, B.a0[2], -B.b0[2]), s1z = fmaf(pz ? hi.z : lo.z, B.a1[2], -B.b1[2]);
+    float sn = fmax3(s0x, s0y, fmaxf(s0z, B.s_lo));
+    float sf = fmin3(s1x, s1y, fminf(s1z, B.s_hi));
+    return sn <= sf;
+}
+
+// One lane's shadow segments of a group: origin x (the receiver), direction
+// d_k = (y_k - x)/|y_k - x|, t in (eps, |y_k - x| - eps)  (O9).
+struct Segs {
+    f3 d[kGroup];
+    float tmax[kGroup];
+    unsigned pend;   // bit k: segment k still unresolved
+    unsigned occ;    // bit k: segment k occluded
+};
+
+// exact MT (O9) of the pending segments of one lane against one triangle;
+// the origin-only terms s = x - v0, q = s x e1, e2.q are shared (identical
+// operations to mt_hit, so identical bits)
+template <bool kCount>
+__device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, float tmin, float4 a, float4 b,
+                                            float4 c, TravStats* st) {
+    const f3 v0 = xyz(a), e1 = xyz(b), e2 = xyz(c);
+    const f3 s = o - v0;
+    const f3 q = cross(s, e1);
+    const float tq = dot(e2, q);
+    unsigned hit = 0;
+#pragma unroll
+    for (int k = 0; k < kGroup; ++k) {
+        if (mask & (1u << k)) {
+            if (kCount) st->tris += 1;
+            const f3 d = S.d[k];
+            const f3 pv = cross(d, e2);
+            const float det = dot(e1, pv);
+            const float inv = 1.0f / det;
+            const float u = dot(s, pv) * inv;
+            const float v = dot(d, q) * inv;
+            const float t = tq * inv;
+            if ((det != 0.0f) & (u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) & (t > tmin) &
+                (t < S.tmax[k]))
+                hit |= 1u << k;
+        }
+    }
+    return hit;
+}
+
+template <bool kCount>
+__device__ __forceinline__ void test_tri(const BvhView& bv, f3 x, Segs& S, float tmin, int tri, OccluderCache& cache,
+                                         TravStats* st) {
+    const unsigned m = S.pend;
+    if (m) {
+        const float4* tr = bv.tris + 3 * tri;
+        unsigned h = mt_segs<kCount>(x, S, m, tmin, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), st);
+        if (h) {
+            S.occ |= h;
+            S.pend &= ~h;
+            cache.found(tri);
+        }
+    }
+}
+
+// Build the beam of the segments in `want` (bit k per lane; the group's
+// VPL positions yk are uniform).  Returns false if the beam is loose.
+__device__ __forceinline__ bool make_beam(f3 x, const f3* yk, unsigned want, unsigned kset, float eps, Beam& B) {
+    const float inf = __int_as_float(0x7f800000);
+    float dn[3] = {inf, inf, inf}, dm[3] = {-inf, -inf, -inf};
+    float yl[3] = {inf, inf, inf}, yh[3] = {-inf, -inf, -inf};
+    float l2n = inf, l2m = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kGroup; ++k) {
+        if (kset & (1u << k)) {   // uniform: VPL k takes part in the beam
+            yl[0] = fminf(yl[0], yk[k].x); yh[0] = fmaxf(yh[0], yk[k].x);
+            yl[1] = fminf(yl[1], yk[k].y); yh[1] = fmaxf(yh[1], yk[k].y);
+            yl[2] = fminf(yl[2], yk[k].z); yh[2] = fmaxf(yh[2], yk[k].z);
+        }
+        if (want & (1u << k)) {
+            f3 D = x - yk[k];
+            dn[0] = fminf(dn[0], D.x); dm[0] = fmaxf(dm[0], D.x);
+            dn[1] = fminf(dn[1], D.y); dm[1] = fmaxf(dm[1], D.y);
+            dn[2] = fminf(dn[2], D.z); dm[2] = fmaxf(dm[2], D.z);
+            float l2 = dot(D, D);
+            l2n = fminf(l2n, l2); l2m = fmaxf(l2m, l2);
+        }
+    }
+    float Dn[3], Dm[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        Dn[a] = fkey_inv(__reduce_min_sync(0xFFFFFFFFu, fkey(dn[a])));
+        Dm[a] = fkey_inv(__reduce_max_sync(0xFFFFFFFFu, fkey(dm[a])));
+    }
+    // l2 >= 0: int order = float order
+    const float lmin = sqrtf(__int_as_float(__reduce_min_sync(0xFFFFFFFFu, __float_as_int(l2n))));
+    const float lmax = sqrtf(__int_as_float(__reduce_max_sync(0xFFFFFFFFu, __float_as_int(l2m))));
+    const float spread = fmax3(Dm[0] - Dn[0], Dm[1] - Dn[1], Dm[2] - Dn[2]);
+    bool tight = spread < kConeSpread * lmin;
+    B.pos = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const bool p = Dn[a] > 0.0f, n = Dm[a] < 0.0f;
+        tight &= p | n;
+        if (p) B.pos |= 1u << a;
+        const float rmax = 1.0f / Dm[a], rmin = 1.0f / Dn[a];
+        B.a0[a] = p ? rmax : rmin;
+        B.b0[a] = (p ? yh[a] : yl[a]) * B.a0[a];
+        B.a1[a] = p ? rmin : rmax;
+        B.b1[a] = (p ? yl[a] : yh[a]) * B.a1[a];
+    }
+    // segment (x_j, y_k) tests t in (eps, L - eps): s = 1 - t/L in (eps/L, 1 - eps/L) within
+    // [eps/Lmax, 1 - eps/Lmax]; half the cap is cut (the rest is slack for MT's rounding of t)
+    B.s_lo = 0.5f * eps / lmax;
+    B.s_hi = 1.0f - B.s_lo;
+    return tight;
+}
+
+// beam traversal (two nodes per step); returns when every lane's S.pend is 0 or the tree is exhausted
+template <bool kCount>
+__device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, float tmin, const Beam& B,
+                                              unsigned dir_neg, OccluderCache& cache, int* __restrict__ sstack,
+                                              TravStats* st) {
+    const int lane = threadIdx.x & 31;
+    const int half = lane >> 4;
+    const unsigned below = (1u << lane) - 1u;
+    const unsigned hmask = half ? 0xFFFF0000u : 0x0000FFFFu;
+    if (bv.root < 0) {  // single-triangle scene
+        test_tri<kCount>(bv, x, S, tmin, 0, cache, st);
+        return;
+    }
+    int sp = 0;
+    int nodeA = bv.root;
+    while (true) {
+        int nodeB = -1;
+        if (sp > 0) nodeB = sstack[--sp];
+        if (kCount && lane == 0) st->wsteps += 1;
+        const int node = half ? nodeB : nodeA;
+        bool hit = false;
+        int ref = INT_MIN, axis = 0;
+        if (node >= 0) {
+            const float4* nd = bv.wide + (int64_t)kWideF4 * node + 2 * (lane & (kWide - 1));
+            const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
+            ref = __float_as_int(lo.w);
+            axis = __float_as_int(hi.w);
+            hit = ref != INT_MIN && beam_box(B, lo, hi);
+        }
+        if (kCount && lane == 0) st->cones += nodeB >= 0 ? 2 * kWide : kWide;
+        const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
+        unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
+        if (Bi) {
+            const int nB = __popc(Bi >> 16), nA = __popc(Bi & 0xFFFFu);
+            const int nh = half ? nB : nA;
+            const int rank = __popc(Bi & below & hmask);
+            const bool rev = (dir_neg >> axis) & 1u;   // segments run x -> y along -axis: visit descending
+            const int pos = (half ? 0 : nB) + (rev ? rank : nh - 1 - rank);   // first to visit ends on top
+            if (hit && ref >= 0) sstack[sp + pos] = ref;
+            sp += nA + nB;
+            __syncwarp();
+        }
+        while (Bl) {
+            const int k = __ffs(Bl) - 1;
+            Bl &= Bl - 1u;
+            const int tri = ~__shfl_sync(0xFFFFFFFFu, ref, k) >> 3;
+            test_tri<kCount>(bv, x, S, tmin, tri, cache, st);
+            if (!__any_sync(0xFFFFFFFFu, S.pend != 0)) return;
+        }
+        if (sp == 0) return;
+        nodeA = sstack[--sp];
+    }
+}
+
+// Resolve the pending segments of a group: beam over the group, else one beam
+// per VPL, else per-ray packets.  yk: the group's VPL positions (uniform).
+template <bool kCount>
+__device__ __forceinline__ void resolve_group(const BvhView& bv, f3 x, Segs& S, float eps, const f3* yk, int g,
+                                              OccluderCache& cache, int* __restrict__ sstack, TravStats* st) {
+    const int lane = threadIdx.x & 31;
+    unsigned kany = 0;   // VPLs with a pending segment in some lane (uniform)
+#pragma unroll
+    for (int k = 0; k < kGroup; ++k)
+        if (__any_sync(0xFFFFFFFFu, (S.pend >> k) & 1u)) kany |= 1u << k;
+    if (!kany) return;
+    const unsigned had = S.occ;
+    if (kCount && lane == 0) st->wrays += 1;
+    Beam B;
+    if (make_beam(x, yk, S.pend, kany, eps, B)) {
+        if (kCount && lane == 0) st->cpk += 1;
+        beam_traverse<kCount>(bv, x, S, eps, B, B.pos, cache, sstack, st);
+    } else {
+        // loose: one beam per VPL of the group, loose single beams go per ray
+        const bool several = __popc(kany) > 1;
+        const unsigned all = S.pend;
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k) {
+            if (!(kany & (1u << k))) continue;                      // uniform
+            S.pend = all & (1u << k);
+            if (several && make_beam(x, yk, S.pend, 1u << k, eps, B)) {
+                if (kCount && lane == 0) st->cpk += 1;
+                beam_traverse<kCount>(bv, x, S, eps, B, B.pos, cache, sstack, st);
+            } else {
+                if (kCount && lane == 0) st->rpk += 1;
+                // per-ray packet traversal of the 4-wide BVH for segment k
+                Ray r;
+                r.o = x; r.d = S.d[k]; r.tmin = eps; r.tmax = S.tmax[k];
+                const bool live = S.pend != 0;
+                const int leader = __ffs(__ballot_sync(0xFFFFFFFFu, live)) - 1;
+                const unsigned neg = (r.d.x < 0.0f ? 1u : 0u) | (r.d.y < 0.0f ? 2u : 0u) | (r.d.z < 0.0f ? 4u : 0u);
+                const unsigned dn = __shfl_sync(0xFFFFFFFFu, neg, leader);
+                if (warp_traverse_ray<kCount>(bv, r, live, false, cache, dn, sstack, st) && live) S.occ |= 1u << k;
+            }
+        }
+    }
+    S.pend = 0;
+    // share the newest occluder found in this resolution with the whole warp
+    const unsigned fresh = __ballot_sync(0xFFFFFFFFu, (S.occ & ~had) != 0);
+    if (fresh) cache.warp = __shfl_sync(0xFFFFFFFFu, cache.own0, __ffs(fresh) - 1);
+}
+
+// The VPL group starting at i (uniform): the longest run of <= kGroup VPLs in
+// [i, iend) whose position box stays within kGroupTol x the distance from
+// the first VPL to the warp's reference receiver xr.
+__device__ __forceinline__ int group_at(const vpl_record* __restrict__ vpls, int i, int iend, f3 xr, f3* yk) {
+    const float4* p = (const float4*)(vpls + i);
+    float4 a = __ldg(p);
+    yk[0] = xyz(a);
+    f3 lo = yk[0], hi = yk[0];
+    f3 dr = yk[0] - xr;
+    const float lim = kGroupTol * sqrtf(dot(dr, dr));
+    int g = 1;
+#pragma unroll
+    for (int k = 1; k < kGroup; ++k) {
+        if (g == k && i + k < iend) {
+            float4 b = __ldg(p + 3 * k);
+            f3 y = xyz(b);
+            f3 l2 = mk3(fminf(lo.x, y.x), fminf(lo.y, y.y), fminf(lo.z, y.z));
+            f3 h2 = mk3(fmaxf(hi.x, y.x), fmaxf(hi.y, y.y), fmaxf(hi.z, y.z));
+            if (fmax3(h2.x - l2.x, h2.y - l2.y, h2.z - l2.z) < lim) {
+                yk[k] = y; lo = l2; hi = h2; g = k + 1;
+            }
+        }
+    }
+    return g;
+}
+
+// One group for one lane: Eq. 1 terms (O13, exact fp32 order), segment
+// setup (O9), cache, traversal.  Returns the traced mask; *vis = traced and
+// unoccluded; w[k] = cx*ci / (r2 * max(r2, b2)) for the visible ones.
+template <bool kCount>
+__device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_record* __restrict__ vpls, int i, int g,
+                                                const f3* yk, f3 x, f3 nx, int tri_x, bool active, float eps,
+                                                float b2, OccluderCache& cache, int* __restrict__ sstack,
+                                                TravStats* st, unsigned* vis, float* w) {
+    Segs S;
+    S.pend = 0; S.occ = 0;
+    unsigned traced = 0;
+#pragma unroll
+    for (int k = 0; k < kGroup; ++k) {
+        w[k] = 0.0f;
+        S.d[k] = mk3(0.0f, 0.0f, 0.0f);
+        S.tmax[k] = 0.0f;
+        if (k < g) {
+            const float4 nb = __ldg((const float4*)(vpls + i + k) + 1);
+            const int tri_i = __float_as_int(__ldg((const float*)(vpls + i + k) + 3));
+            const f3 d = yk[k] - x;
+            const float r2 = dot(d, d);
+            const float cx = dot(nx, d);
+            const float ci = -dot(xyz(nb), d);
+            if (active && tri_i != tri_x && cx > 0.0f && ci > 0.0f) {
+                traced |= 1u << k;
+                w[k] = __fdividef(cx * ci, r2 * fmaxf(r2, b2));
+                const float dist = sqrtf(r2);   // = sqrtf(dot(d, d)) of O9's segment setup
+                S.d[k] = mk3(d.x / dist, d.y / dist, d.z / dist);
+                S.tmax[k] = dist - eps;
+                if (S.tmax[k] > eps) S.pend |= 1u << k;
+            }
+        }
+    }
+    *vis = 0;
+    if (!__any_sync(0xFFFFFFFFu, traced != 0)) return 0;
+    // occluder cache: exact MT against recent occluders
+    if (S.pend && cache.own0 >= 0) test_tri<kCount>(bv, x, S, eps, cache.own0, cache, st);
+    if (S.pend && cache.own1 >= 0) test_tri<kCount>(bv, x, S, eps, cache.own1, cache, st);
+    if (S.pend && cache.warp >= 0 && cache.warp != cache.own0 && cache.warp != cache.own1)
+        test_tri<kCount>(bv, x, S, eps, cache.warp, cache, st);
+    if (kCount) st->chits += __popc(S.occ);
+    resolve_group<kCount>(bv, x, S, eps, yk, g, cache, sstack, st);
+    *vis = traced & ~S.occ;
+    return traced;
+}
+
+}  // namespace vplgi

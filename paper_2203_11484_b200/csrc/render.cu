@@ -1,6 +1,8 @@
 // render.cu — a7 render_gbuffer (O12), a8 gather_indirect (Eq. 1, O13) and
 // the test hooks that share their traversal code.
-#include "common.cuh"
+#include <cub/device/device_radix_sort.cuh>
+
+#include "gather.cuh"
 
 namespace vplgi {
 
@@ -44,38 +46,16 @@ __global__ void k_gbuffer(SceneView sv, BvhView bv, TileMap tm, vpl_gpoint* __re
     gb[pix] = o;
 }
 
-struct VplPos {
-    f3 y, n;
-    int tri;
-};
-__device__ __forceinline__ VplPos load_vpl_geo(const vpl_record* v) {
-    const float4* p = (const float4*)v;
-    float4 a = __ldg(p), b = __ldg(p + 1);
-    VplPos g;
-    g.y = xyz(a); g.tri = __float_as_int(a.w);
-    g.n = xyz(b);
-    return g;
-}
-
-struct VplGeo {
-    f3 y, n, phi;
-    int tri;
-};
-__device__ __forceinline__ VplGeo load_vpl(const vpl_record* v) {
-    const float4* p = (const float4*)v;
-    float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
-    VplGeo g;
-    g.y = xyz(a); g.tri = __float_as_int(a.w);
-    g.n = xyz(b); g.phi = xyz(c);
-    return g;
-}
-
-// a8 — Eq. 1 gather.  One warp per 8x4 pixel block; all lanes walk
-// the VPL list in the same order, so the shadow rays of a warp share their
-// end point (coherent traversal).  fp32 two-level accumulation: a per-batch
-// partial is folded into the running total every 256 VPLs.
+// a8 — Eq. 1 gather.  Persistent: each warp takes 8x4 pixel blocks
+// from an atomic queue; all lanes walk the VPL list in the same order, in
+// groups of nearby VPLs, so the shadow segments of a warp form a narrow beam
+// (gather.cuh).  fp32 two-level accumulation: a per-batch partial is folded
+// into the running total every 256 VPLs (groups never straddle a batch).
+#ifndef VPL_GATHER_MINB
+#define VPL_GATHER_MINB 8
+#endif
 template <bool kCount>
-__global__ void __launch_bounds__(128, 8) k_gather(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb,
+__global__ void __launch_bounds__(128, VPL_GATHER_MINB) k_gather(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb,
                                                 const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
                                                 vpl_counters* __restrict__ ctr, int* __restrict__ queue) {
     __shared__ int s_stack[4][kWarpStack];
@@ -103,29 +83,32 @@ __global__ void __launch_bounds__(128, 8) k_gather(SceneView sv, BvhView bv, Til
         OccluderCache cache;
         TravStats st;
         unsigned long long n_traced = 0, n_vis = 0;
-        if (__any_sync(0xFFFFFFFFu, active)) {
+        const unsigned am = __ballot_sync(0xFFFFFFFFu, active);
+        if (am) {
+            const int l0 = __ffs(am) - 1;
+            const f3 xr = mk3(__shfl_sync(0xFFFFFFFFu, x.x, l0), __shfl_sync(0xFFFFFFFFu, x.y, l0),
+                              __shfl_sync(0xFFFFFFFFu, x.z, l0));
             for (int i0 = 0; i0 < M; i0 += 256) {
                 float part[3] = {0.0f, 0.0f, 0.0f};
-                int i1 = min(M, i0 + 256);
-                for (int i = i0; i < i1; ++i) {
-                    VplPos v = load_vpl_geo(vpls + i);
-                    f3 d = v.y - x;
-                    float r2 = dot(d, d);
-                    float cx = dot(nx, d);
-                    float ci = -dot(v.n, d);
-                    bool traced = active && v.tri != tri_x && cx > 0.0f && ci > 0.0f;
-                    if (!__any_sync(0xFFFFFFFFu, traced)) continue;       // warp-uniform skip
-                    Ray ray;
-                    bool live = traced && seg_ray(x, v.y, eps, ray);
-                    bool occl = warp_any_hit<kCount>(bv, ray, v.y, eps, live, cache, sstack, &st);
-                    if (kCount && traced) ++n_traced;
-                    if (!traced || occl) continue;
-                    if (kCount) ++n_vis;
-                    float w = __fdividef(cx * ci, r2 * fmaxf(r2, b2));
-                    float4 phi = __ldg((const float4*)(vpls + i) + 2);
-                    part[0] = fmaf(phi.x, w, part[0]);
-                    part[1] = fmaf(phi.y, w, part[1]);
-                    part[2] = fmaf(phi.z, w, part[2]);
+                const int i1 = min(M, i0 + 256);
+                for (int i = i0; i < i1;) {
+                    f3 yk[kGroup];
+                    const int gsz = group_at(vpls, i, i1, xr, yk);
+                    unsigned vis;
+                    float w[kGroup];
+                    const unsigned tr = shade_group<kCount>(bv, vpls, i, gsz, yk, x, nx, tri_x, active, eps, b2, cache,
+                                                            sstack, &st, &vis, w);
+                    if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
+#pragma unroll
+                    for (int k = 0; k < kGroup; ++k) {
+                        if (vis & (1u << k)) {
+                            const float4 phi = __ldg((const float4*)(vpls + i + k) + 2);
+                            part[0] = fmaf(phi.x, w[k], part[0]);
+                            part[1] = fmaf(phi.y, w[k], part[1]);
+                            part[2] = fmaf(phi.z, w[k], part[2]);
+                        }
+                    }
+                    i += gsz;
                 }
                 acc[0] += part[0]; acc[1] += part[1]; acc[2] += part[2];
             }
@@ -153,39 +136,40 @@ __global__ void __launch_bounds__(128, 8) k_gather(SceneView sv, BvhView bv, Til
 }
 
 // test hook: traced / visible bits of listed pixels x all VPLs, through the
-// gather's own warp-cooperative traversal (lanes = 32 consecutive listed pixels)
+// gather's own group / beam traversal (lanes = 32 consecutive listed pixels)
 __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict__ gb, const vpl_record* __restrict__ vpls,
                           int32_t M, const int32_t* __restrict__ pixels, int32_t n_px, uint32_t* __restrict__ tbits,
                           uint32_t* __restrict__ vbits) {
     __shared__ int s_stack[2][kWarpStack];
     int* sstack = s_stack[threadIdx.x >> 5];
     int64_t words = (M + 31) / 32;
-    int lane = threadIdx.x & 31;
     OccluderCache cache;
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
     if ((k - lane) >= n_px) return;                      // whole warp out of range
     bool inb = k < n_px;
-    const vpl_gpoint* g = gb + (inb ? pixels[k] : 0);
-    bool active = inb && g->tri >= 0 && g->front;
-    f3 x = ld3(g->pos), nx = ld3(g->nrm);
-    int tri_x = g->tri;
-    float eps = sv.hdr->eps;
+    const vpl_gpoint* gp = gb + (inb ? pixels[k] : 0);
+    bool active = inb && gp->tri >= 0 && gp->front;
+    f3 x = ld3(gp->pos), nx = ld3(gp->nrm);
+    int tri_x = gp->tri;
+    const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
+    const unsigned am = __ballot_sync(0xFFFFFFFFu, active);
+    const int l0 = am ? __ffs(am) - 1 : 0;
+    const f3 xr = mk3(__shfl_sync(0xFFFFFFFFu, x.x, l0), __shfl_sync(0xFFFFFFFFu, x.y, l0),
+                      __shfl_sync(0xFFFFFFFFu, x.z, l0));
     for (int64_t wd = 0; wd < words; ++wd) {
         uint32_t tb = 0, vb = 0;
-        for (int b = 0; b < 32; ++b) {
-            int i = (int)(wd * 32 + b);
-            if (i >= M) break;
-            VplGeo v = load_vpl(vpls + i);
-            f3 d = v.y - x;
-            float cx = dot(nx, d);
-            float ci = -dot(v.n, d);
-            bool traced = active && v.tri != tri_x && cx > 0.0f && ci > 0.0f;
-            if (!__any_sync(0xFFFFFFFFu, traced)) continue;
-            Ray ray;
-            bool live = traced && seg_ray(x, v.y, eps, ray);
-            bool occl = warp_any_hit<false>(bv, ray, v.y, eps, live, cache, sstack, nullptr);
-            if (traced) tb |= 1u << b;
-            if (traced && !occl) vb |= 1u << b;
+        const int i0 = (int)(wd * 32), i1 = min(M, i0 + 32);
+        for (int i = i0; i < i1;) {
+            f3 yk[kGroup];
+            const int gsz = group_at(vpls, i, i1, xr, yk);
+            unsigned vis;
+            float w[kGroup];
+            const unsigned tr = shade_group<false>(bv, vpls, i, gsz, yk, x, nx, tri_x, active, eps, b2, cache, sstack,
+                                                   nullptr, &vis, w);
+            tb |= tr << (i - i0);
+            vb |= vis << (i - i0);
+            i += gsz;
         }
         if (inb) { tbits[k * words + wd] = tb; vbits[k * words + wd] = vb; }
     }
@@ -219,6 +203,81 @@ __global__ void k_philox_batch(const uint32_t* __restrict__ in, int64_t n, uint3
 }
 
 static inline int nb(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+// Gather-side VPL order: Eq. 1 is a sum over the VPL set, so the gather may
+// visit the VPLs in any fixed order.  It visits them in Morton order of
+// their positions (30-bit code over the VPL bounding box) so consecutive
+// VPLs are close: the occluder cache hits more often and groups of nearby
+// VPLs share one beam (gather.cuh).  The array order of vpl_generate_vpls
+// (the oracle-checked output) is not touched; the sorted copy lives in the
+// gather's work buffer.
+__device__ __forceinline__ uint32_t spread10(uint32_t x) {
+    x &= 0x3FFu;
+    x = (x | (x << 16)) & 0x030000FFu;
+    x = (x | (x << 8)) & 0x0300F00Fu;
+    x = (x | (x << 4)) & 0x030C30C3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+}
+__global__ void k_vpl_bbox(const vpl_record* __restrict__ v, int32_t M, unsigned* __restrict__ box) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const float* p = (const float*)(v + i);
+    for (int a = 0; a < 3; ++a) {
+        atomicMin(box + a, (unsigned)fkey(p[a]) ^ 0x80000000u);
+        atomicMax(box + 3 + a, (unsigned)fkey(p[a]) ^ 0x80000000u);
+    }
+}
+__global__ void k_vpl_morton(const vpl_record* __restrict__ v, int32_t M, const unsigned* __restrict__ box,
+                             uint32_t* __restrict__ keys, int32_t* __restrict__ idx) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const float* p = (const float*)(v + i);
+    uint32_t c = 0;
+    for (int a = 0; a < 3; ++a) {
+        float lo = fkey_inv((int)(box[a] ^ 0x80000000u)), hi = fkey_inv((int)(box[3 + a] ^ 0x80000000u));
+        float ext = hi - lo;
+        float q = ext > 0.0f ? (p[a] - lo) * (1024.0f / ext) : 0.0f;
+        c |= spread10(min((uint32_t)fmaxf(q, 0.0f), 1023u)) << a;
+    }
+    keys[i] = c;
+    idx[i] = i;
+}
+__global__ void k_vpl_permute(const vpl_record* __restrict__ v, const int32_t* __restrict__ idx, int32_t M,
+                              vpl_record* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const float4* src = (const float4*)(v + idx[i]);
+    float4* dst = (float4*)(out + i);
+    dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2];
+}
+
+struct GatherWork {
+    int* queue;
+    unsigned* box;
+    uint32_t *keys, *keys2;
+    int32_t *idx, *idx2;
+    vpl_record* sorted;
+    void* cub;
+    size_t cub_bytes;
+};
+static size_t gather_layout(int32_t M, char* base, GatherWork* w) {
+    Bump b{base};
+    w->queue = b.take<int>(1);
+    w->box = b.take<unsigned>(6);
+    size_t m = (size_t)(M > 0 ? M : 1);
+    w->keys = b.take<uint32_t>(m);
+    w->keys2 = b.take<uint32_t>(m);
+    w->idx = b.take<int32_t>(m);
+    w->idx2 = b.take<int32_t>(m);
+    w->sorted = b.take<vpl_record>(m);
+    size_t c = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, (int)m, 0, 30);
+    w->cub_bytes = c;
+    w->cub = b.take<char>(c);
+    return b.off;
+}
 
 static int32_t make_tilemap(const SceneHdr& hh, const int32_t* d_tiles, int32_t n_tiles, int32_t tw, int32_t th,
                             TileMap* tm) {
@@ -257,9 +316,10 @@ int32_t vpl_render_gbuffer(const void* d_scene, const void* d_bvh, const int32_t
     return VPL_OK;
 }
 
-int32_t vpl_gather_bytes(size_t* work_bytes) {
-    if (!work_bytes) return VPL_EINVAL;
-    *work_bytes = 256;
+int32_t vpl_gather_bytes(int32_t n_vpls, size_t* work_bytes) {
+    if (!work_bytes || n_vpls < 0) return VPL_EINVAL;
+    GatherWork w;
+    *work_bytes = gather_layout(n_vpls, nullptr, &w);
     return VPL_OK;
 }
 
@@ -270,25 +330,44 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
         set_error("vpl_gather_indirect: bad arguments");
         return VPL_EINVAL;
     }
-    if (work_bytes < 256) { set_error("vpl_gather_indirect: work too small"); return VPL_ESMALL; }
+    GatherWork w;
+    if (work_bytes < gather_layout(n_vpls, nullptr, &w)) {
+        set_error("vpl_gather_indirect: work buffer smaller than vpl_gather_bytes(n_vpls)");
+        return VPL_ESMALL;
+    }
+    gather_layout(n_vpls, (char*)d_work, &w);
     cudaStream_t s = (cudaStream_t)stream;
     SceneHdr hh;
     VPL_TRY(read_scene_hdr(d_scene, s, &hh));
     TileMap tm;
     VPL_TRY(make_tilemap(hh, d_tiles, n_tiles, tile_w, tile_h, &tm));
     if (n_tiles == 0) return VPL_OK;
-    int* queue = (int*)d_work;
+    int* queue = w.queue;
     VPL_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
+    const vpl_record* vp = d_vpls;
+    if (n_vpls > 1) {
+        const unsigned init[6] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u};
+        VPL_CUDA(cudaMemcpyAsync(w.box, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        k_vpl_bbox<<<nb(n_vpls, 256), 256, 0, s>>>(d_vpls, n_vpls, w.box);
+        VPL_LAUNCHED("k_vpl_bbox");
+        k_vpl_morton<<<nb(n_vpls, 256), 256, 0, s>>>(d_vpls, n_vpls, w.box, w.keys, w.idx);
+        VPL_LAUNCHED("k_vpl_morton");
+        size_t cb = w.cub_bytes;
+        VPL_CUDA(cub::DeviceRadixSort::SortPairs(w.cub, cb, w.keys, w.keys2, w.idx, w.idx2, n_vpls, 0, 30, s));
+        k_vpl_permute<<<nb(n_vpls, 256), 256, 0, s>>>(d_vpls, w.idx2, n_vpls, w.sorted);
+        VPL_LAUNCHED("k_vpl_permute");
+        vp = w.sorted;
+    }
     int dev = 0, sms = 148;
     VPL_CUDA(cudaGetDevice(&dev));
     VPL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    int grid = sms * 8;  // persistent: 8 CTAs x 4 warps per SM
+    int grid = sms * VPL_GATHER_MINB;  // persistent: VPL_GATHER_MINB CTAs x 4 warps per SM
     SceneView sv = scene_view(d_scene, hh.n);
     BvhView bv = bvh_view(d_bvh, hh.n);
     if (d_ctr)
-        k_gather<true><<<grid, 128, 0, s>>>(sv, bv, tm, d_gbuf, d_vpls, n_vpls, d_rgb, d_ctr, queue);
+        k_gather<true><<<grid, 128, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue);
     else
-        k_gather<false><<<grid, 128, 0, s>>>(sv, bv, tm, d_gbuf, d_vpls, n_vpls, d_rgb, nullptr, queue);
+        k_gather<false><<<grid, 128, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue);
     VPL_LAUNCHED("k_gather");
     return VPL_OK;
 }
