@@ -94,13 +94,15 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- algorithmic op counts
-# Per-unit thread-op counts (FMA + ALU + MUFU pipe instructions per unit of
-# algorithmic work, restated and extended in DESIGN.md §5)
-OPS = {"pairs": 14,        # d = y - x, r^2, two dots, cosine cull, self test
-       "traced": 20,       # segment setup (sqrt, 3 div), geometry term, 3 FMA accumulate
-       "box_tests": 17,    # per-ray slab test, centre/half-extent form (12 FMA-pipe + 5 ALU)
-       "cone_tests": 35,   # packet-cone x box interval test (18 FMA-pipe + 17 ALU)
-       "tri_tests": 35}    # exact Moller-Trumbore (27 FMA-pipe + 7 ALU + 1 MUFU)
+# Per-unit thread-op counts: the arithmetic the method itself prescribes per
+# unit of work.  The exact fp32 contract (O0) forbids FMA
+# contraction in the Eq. 1 terms and in Moller-Trumbore, so those count as
+# separate FMUL/FADD; divisions and square roots count as one op each.
+OPS = {"pairs": 21,        # d = y - x (3), r^2 (5), cx (5), ci (5), tri / cx / ci tests (3)   (O13)
+       "traced": 13,       # sqrt, 3 div (direction), tmax, tmax > eps, w (4), 3 FFMA accumulate (O9, O13)
+       "box_tests": 17,    # per-ray slab test, centre/half-extent form: 3 FFMA + 3 FMUL + 6 FADD + 4 min/max + 1 cmp
+       "cone_tests": 17,   # beam x child box: 6 FFMA + 6 SEL + 4 min/max + 1 cmp (gather.cuh beam_box)
+       "tri_tests": 52}    # exact Moller-Trumbore (O9): 44 FMUL/FADD + 1 div + 7 compares
 
 
 def algorithmic_ops(c: dict) -> int:

@@ -386,82 +386,13 @@ struct OccluderCache {
     }
 };
 
-// The packet as a cone: every live lane's shadow segment runs from its
-// receiver x_j to the common VPL position y, i.e. y + s * D_j, s in [0, 1],
-// D_j = x_j - y.  With D in the box [Dmin, Dmax], 1/D_a lies in [ilo_a, ihi_a]
-// (= [1/Dmax, 1/Dmin], or (-inf, inf) when D_a changes sign in the packet), so
-// the s-range where a segment can be inside the slab [lo_a, hi_a] is within
-// the hull of the four products (p - y_a) * {ilo_a, ihi_a}, p in {lo_a, hi_a}.
-// A box is culled only if these per-axis ranges and [0, 1] do not meet — no
-// ray of the packet can then enter it (interval arithmetic, conservative; the
-// box padding absorbs the fp32 rounding of the products).
-struct Cone {
-    f3 y, ilo, ihi;
-    float s_lo, s_hi;   // s-range that can hold an occluder of any packet segment (eps caps removed)
-};
-
 __device__ __forceinline__ int fkey(float f) {   // order-preserving float -> int
     int i = __float_as_int(f);
     return i ^ ((i >> 31) & 0x7FFFFFFF);
 }
 __device__ __forceinline__ float fkey_inv(int k) { return __int_as_float(k ^ ((k >> 31) & 0x7FFFFFFF)); }
 
-__device__ __forceinline__ void cone_axis(float dmin, float dmax, float& ilo, float& ihi) {
-    const float inf = __int_as_float(0x7f800000);
-    bool same = dmin > 0.0f || dmax < 0.0f;
-    ilo = same ? 1.0f / dmax : -inf;
-    ihi = same ? 1.0f / dmin : inf;
-}
-
-constexpr float kConeSpread = 0.1f;  // cone traversal iff max_a (Dmax_a - Dmin_a) < kConeSpread * |D|_min
-
-__device__ __forceinline__ Cone make_cone(f3 y, f3 x, bool live, float eps, bool& tight) {
-    f3 D = x - y;
-    const int big = 0x7FFFFFFF, small = (int)0x80000000;
-    int nx = __reduce_min_sync(0xFFFFFFFFu, live ? fkey(D.x) : big);
-    int ny = __reduce_min_sync(0xFFFFFFFFu, live ? fkey(D.y) : big);
-    int nz = __reduce_min_sync(0xFFFFFFFFu, live ? fkey(D.z) : big);
-    int mx = __reduce_max_sync(0xFFFFFFFFu, live ? fkey(D.x) : small);
-    int my = __reduce_max_sync(0xFFFFFFFFu, live ? fkey(D.y) : small);
-    int mz = __reduce_max_sync(0xFFFFFFFFu, live ? fkey(D.z) : small);
-    Cone c;
-    c.y = y;
-    float dnx = fkey_inv(nx), dny = fkey_inv(ny), dnz = fkey_inv(nz);
-    float dmx = fkey_inv(mx), dmy = fkey_inv(my), dmz = fkey_inv(mz);
-    float spread = fmax3(dmx - dnx, dmy - dny, dmz - dnz);
-    // |D| of the leader lane bounds the lengths up to the spread
-    float l2 = dot(D, D);
-    float lmin = sqrtf(__int_as_float(__reduce_min_sync(0xFFFFFFFFu, live ? __float_as_int(l2) : 0x7F800000)));
-    bool straddle = !(dnx > 0.0f || dmx < 0.0f) || !(dny > 0.0f || dmy < 0.0f) || !(dnz > 0.0f || dmz < 0.0f);
-    tight = !straddle && spread < kConeSpread * lmin;
-    // Segment j only tests t in (eps, |D_j| - eps), i.e. s = 1 - t/|D_j| in (eps/|D_j|, 1 - eps/|D_j|),
-    // inside [eps/|D|max, 1 - eps/|D|max].  Half of that cap is cut off (the other half is slack for
-    // the rounding of the exact MT t), which culls the receiver's and the VPL's own surfaces.
-    float lmax = sqrtf(__int_as_float(__reduce_max_sync(0xFFFFFFFFu, live ? __float_as_int(l2) : 0)));
-    c.s_lo = 0.5f * eps / lmax;
-    c.s_hi = 1.0f - c.s_lo;
-    cone_axis(fkey_inv(nx), fkey_inv(mx), c.ilo.x, c.ihi.x);
-    cone_axis(fkey_inv(ny), fkey_inv(my), c.ilo.y, c.ihi.y);
-    cone_axis(fkey_inv(nz), fkey_inv(mz), c.ilo.z, c.ihi.z);
-    return c;
-}
-
-__device__ __forceinline__ void cone_slab(float lo, float hi, float y, float ilo, float ihi, float& s0, float& s1) {
-    float pl = lo - y, ph = hi - y;
-    float a = pl * ilo, b = pl * ihi, c = ph * ilo, d = ph * ihi;
-    s0 = fminf(fmin3(a, b, c), d);
-    s1 = fmaxf(fmax3(a, b, c), d);
-}
-
-__device__ __forceinline__ bool cone_box(const Cone& k, float4 lo, float4 hi) {
-    float x0, x1, y0, y1, z0, z1;
-    cone_slab(lo.x, hi.x, k.y.x, k.ilo.x, k.ihi.x, x0, x1);
-    cone_slab(lo.y, hi.y, k.y.y, k.ilo.y, k.ihi.y, y0, y1);
-    cone_slab(lo.z, hi.z, k.y.z, k.ilo.z, k.ihi.z, z0, z1);
-    float sn = fmax3(x0, y0, fmaxf(z0, k.s_lo));
-    float sf = fmin3(x1, y1, fminf(z1, k.s_hi));
-    return sn <= sf;
-}
+constexpr float kConeSpread = 0.1f;  // beam traversal iff max_a (Dmax_a - Dmin_a) < kConeSpread * |D|_min
 
 // Per-ray packet traversal of the 4-wide BVH: every live lane tests its own
 // ray against the 4 children; a child is entered if any lane's ray enters it.
@@ -536,127 +467,6 @@ __device__ __forceinline__ bool warp_traverse_ray(const BvhView& bv, Ray r, bool
         if (sp == 0) break;
         node = sstack[--sp];
     }
-    return occl;
-}
-
-// Cone traversal of the kWide-wide BVH (kWide = 16, leaves = single
-// triangles).  Each step pops up to two nodes: lanes 0-15 test the children of
-// the first against the packet cone, lanes 16-31 those of the second.  Hit
-// triangle children are resolved at once — every live lane runs the exact MT
-// test of its own ray (O9) — and hit inner children are pushed onto the
-// warp-uniform shared-memory stack, the first node's children on top in
-// visiting order (the order differs from a one-node-per-step depth-first
-// traversal only in that the second node is opened early).  Must be called by all 32 lanes.  A lane may test triangles its
-// own ray would have culled; that cannot change an any-hit result, so each
-// lane's answer equals bvh_any_hit's.
-template <bool kCount>
-__device__ __forceinline__ bool warp_traverse_cone(const BvhView& bv, const Ray& r, bool live, bool occl,
-                                              OccluderCache& cache, const Cone& cone, unsigned dir_neg,
-                                              int* __restrict__ sstack, TravStats* st) {
-    const int lane = threadIdx.x & 31;
-    const int half = lane >> 4;
-    const unsigned below = (1u << lane) - 1u;
-    const unsigned hmask = half ? 0xFFFF0000u : 0x0000FFFFu;
-    if (bv.root < 0) {  // single-triangle scene
-        const float4* tr = bv.tris;
-        float t;
-        bool hitt = mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t) & live & !occl;
-        if (kCount && live && !occl) st->tris += 1;
-        if (hitt) { occl = true; cache.found(0); }
-        return occl;
-    }
-    int sp = 0;
-    int nodeA = bv.root;
-    while (true) {
-        int nodeB = -1;
-        if (sp > 0) nodeB = sstack[--sp];
-        if (kCount && lane == 0) st->wsteps += 1;
-        const int node = half ? nodeB : nodeA;
-        bool hit = false;
-        int ref = INT_MIN;
-        int axis = 0;
-        if (node >= 0) {
-            const float4* nd = bv.wide + (int64_t)kWideF4 * node + 2 * (lane & (kWide - 1));
-            float4 lo = __ldg(nd), hi = __ldg(nd + 1);
-            ref = __float_as_int(lo.w);
-            axis = __float_as_int(hi.w);
-            hit = ref != INT_MIN && cone_box(cone, lo, hi);
-        }
-        if (kCount && lane == 0) st->cones += nodeB >= 0 ? 2 * kWide : kWide;
-        const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
-        unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
-        if (Bi) {
-            const int nB = __popc(Bi >> 16), nA = __popc(Bi & 0xFFFFu);
-            const int nh = half ? nB : nA;
-            const int rank = __popc(Bi & below & hmask);
-            const bool rev = (dir_neg >> axis) & 1u;       // packet travels -axis: visit descending
-            const int pos = (half ? 0 : nB) + (rev ? rank : nh - 1 - rank);   // first to visit ends on top
-            if (hit && ref >= 0) sstack[sp + pos] = ref;
-            sp += nA + nB;
-            __syncwarp();
-        }
-        while (Bl) {
-            const int k = __ffs(Bl) - 1;
-            Bl &= Bl - 1u;
-            const int tri = ~__shfl_sync(0xFFFFFFFFu, ref, k) >> 3;
-            const bool go = live && !occl;
-            const float4* tr = bv.tris + 3 * tri;
-            float t;
-            bool hitt = mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t) & go;
-            if (kCount && go) st->tris += 1;
-            if (hitt) { occl = true; cache.found(tri); }
-            if (!__any_sync(0xFFFFFFFFu, live && !occl)) return occl;
-        }
-        if (sp == 0) break;
-        nodeA = sstack[--sp];
-    }
-    return occl;
-}
-
-template <bool kCount>
-__device__ __forceinline__ bool cached_occluder(const BvhView& bv, const Ray& r, int tri, TravStats* st) {
-    const float4* tr = bv.tris + 3 * tri;
-    float t;
-    if (kCount) st->tris += 1;
-    return mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t);
-}
-
-// Warp-cooperative any-hit for a packet of shadow segments x_j -> y sharing
-// the end point y (one VPL, 32 receivers).  First the exact MT tests of
-// recently found occluders (consecutive VPLs are spatially coherent: Morton
-// order), then the cone traversal for the lanes still unresolved.
-template <bool kCount>
-__device__ __forceinline__ bool warp_any_hit(const BvhView& bv, const Ray& r, f3 y, float eps, bool live,
-                                             OccluderCache& cache, int* __restrict__ sstack, TravStats* st) {
-    bool occl = false;
-    if (live && cache.own0 >= 0) occl = cached_occluder<kCount>(bv, r, cache.own0, st);
-    if (live && !occl && cache.own1 >= 0) occl = cached_occluder<kCount>(bv, r, cache.own1, st);
-    if (live && !occl && cache.warp >= 0 && cache.warp != cache.own0 && cache.warp != cache.own1) {
-        occl = cached_occluder<kCount>(bv, r, cache.warp, st);
-        if (occl) cache.found(cache.warp);
-    }
-    bool need_lane = live && !occl;
-    if (kCount && live && occl) st->chits += 1;
-    // (the per-ray fallback derives its own slab fields)
-    bool cone_tight;
-    unsigned need = __ballot_sync(0xFFFFFFFFu, need_lane);
-    if (!need) return occl;
-    int leader = __ffs(need) - 1;
-    unsigned neg = (r.d.x < 0.0f ? 1u : 0u) | (r.d.y < 0.0f ? 2u : 0u) | (r.d.z < 0.0f ? 4u : 0u);
-    const unsigned dir_neg = __shfl_sync(0xFFFFFFFFu, neg, leader);
-    if (kCount && (threadIdx.x & 31) == 0) st->wrays += 1;
-    Cone cone = make_cone(y, r.o, need_lane, eps, cone_tight);
-    bool was = occl;
-    if (cone_tight)
-        occl = warp_traverse_cone<kCount>(bv, r, live, occl, cache, cone, dir_neg, sstack, st);
-    else
-        occl = warp_traverse_ray<kCount>(bv, r, live, occl, cache, dir_neg, sstack, st);
-    if (kCount && (threadIdx.x & 31) == 0) {
-        if (cone_tight) st->cpk += 1; else st->rpk += 1;
-    }
-    // share the newest occluder found in this traversal with the whole warp
-    unsigned fresh = __ballot_sync(0xFFFFFFFFu, occl && !was);
-    if (fresh) cache.warp = __shfl_sync(0xFFFFFFFFu, cache.own0, __ffs(fresh) - 1);
     return occl;
 }
 

@@ -46,6 +46,12 @@ constexpr float kGroupTol = VPL_GROUP_TOL; // group iff the VPL box extent < tol
 // actual segments).  Stored as s0 = N*a0 - b0, s1 = F*a1 - b1 with N/F the
 // box face picked by the sign of D_a; evaluated with one FFMA each.  The
 // rounding (position error ~ulp(coord)) is absorbed by the box padding.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 struct Beam {
     float a0[3], b0[3], a1[3], b1[3];
     float s_lo, s_hi;
@@ -156,7 +162,9 @@ __device__ __forceinline__ bool make_beam(f3 x, const f3* yk, unsigned want, uns
         const bool p = Dn[a] > 0.0f, n = Dm[a] < 0.0f;
         tight &= p | n;
         if (p) B.pos |= 1u << a;
-        const float rmax = 1.0f / Dm[a], rmin = 1.0f / Dn[a];
+        // approximate reciprocals: a0 and b0 = y*a0 share the same a0, so s is scaled by
+        // (1 + 2^-22) at most — a position error far below the box padding
+        const float rmax = rcp_approx(Dm[a]), rmin = rcp_approx(Dn[a]);
         B.a0[a] = p ? rmax : rmin;
         B.b0[a] = (p ? yh[a] : yl[a]) * B.a0[a];
         B.a1[a] = p ? rmin : rmax;
@@ -182,23 +190,24 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
         test_tri<kCount>(bv, x, S, tmin, 0, cache, st);
         return;
     }
-    int sp = 0;
-    int nodeA = bv.root;
-    while (true) {
-        int nodeB = -1;
-        if (sp > 0) nodeB = sstack[--sp];
-        if (kCount && lane == 0) st->wsteps += 1;
-        const int node = half ? nodeB : nodeA;
+    // the stack holds inner nodes only; each step pops the top two (lanes 0-15 take the top one)
+    if (lane == 0) sstack[0] = bv.root;
+    __syncwarp();
+    int sp = 1;
+    while (sp > 0) {
+        const int idx = sp - 1 - half;
+        const int node = idx >= 0 ? sstack[idx] : -1;
+        if (kCount && lane == 0) { st->wsteps += 1; st->cones += sp >= 2 ? 2 * kWide : kWide; }
+        sp = max(sp - 2, 0);
         bool hit = false;
         int ref = INT_MIN, axis = 0;
         if (node >= 0) {
-            const float4* nd = bv.wide + (int64_t)kWideF4 * node + 2 * (lane & (kWide - 1));
+            const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)node << 9) + ((lane & (kWide - 1)) << 5));
             const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
             ref = __float_as_int(lo.w);
             axis = __float_as_int(hi.w);
             hit = ref != INT_MIN && beam_box(B, lo, hi);
         }
-        if (kCount && lane == 0) st->cones += nodeB >= 0 ? 2 * kWide : kWide;
         const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
         unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
         if (Bi) {
@@ -209,8 +218,8 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
             const int pos = (half ? 0 : nB) + (rev ? rank : nh - 1 - rank);   // first to visit ends on top
             if (hit && ref >= 0) sstack[sp + pos] = ref;
             sp += nA + nB;
-            __syncwarp();
         }
+        __syncwarp();
         while (Bl) {
             const int k = __ffs(Bl) - 1;
             Bl &= Bl - 1u;
@@ -218,8 +227,6 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
             test_tri<kCount>(bv, x, S, tmin, tri, cache, st);
             if (!__any_sync(0xFFFFFFFFu, S.pend != 0)) return;
         }
-        if (sp == 0) return;
-        nodeA = sstack[--sp];
     }
 }
 

@@ -51,16 +51,19 @@ __global__ void k_gbuffer(SceneView sv, BvhView bv, TileMap tm, vpl_gpoint* __re
 // groups of nearby VPLs, so the shadow segments of a warp form a narrow beam
 // (gather.cuh).  fp32 two-level accumulation: a per-batch partial is folded
 // into the running total every 256 VPLs (groups never straddle a batch).
-#ifndef VPL_GATHER_MINB
-#define VPL_GATHER_MINB 8
+// One warp per CTA: the traversal stack is then at a fixed shared-memory
+// address (no per-warp base to keep live in a register), and 32 one-warp
+// CTAs fill an SM at the 64-register budget.
+#ifndef VPL_GATHER_CTAS
+#define VPL_GATHER_CTAS 32
 #endif
 template <bool kCount>
-__global__ void __launch_bounds__(128, VPL_GATHER_MINB) k_gather(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb,
+__global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb,
                                                 const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
                                                 vpl_counters* __restrict__ ctr, int* __restrict__ queue) {
-    __shared__ int s_stack[4][kWarpStack];
-    const int lane = threadIdx.x & 31;
-    int* sstack = s_stack[threadIdx.x >> 5];
+    __shared__ int sstack[kWarpStack];
+    __shared__ float s_acc[3][32];   // running per-lane totals (kept out of the register budget)
+    const int lane = threadIdx.x;
     const int64_t nw = tm.n_warps();
     const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
     while (true) {
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(128, VPL_GATHER_MINB) k_gather(SceneView sv, B
             active = tri_x >= 0 && __float_as_int(b.w) != 0;
             x = xyz(a); nx = xyz(b);
         }
-        float acc[3] = {0.0f, 0.0f, 0.0f};
+        s_acc[0][lane] = 0.0f; s_acc[1][lane] = 0.0f; s_acc[2][lane] = 0.0f;
         OccluderCache cache;
         TravStats st;
         unsigned long long n_traced = 0, n_vis = 0;
@@ -110,16 +113,16 @@ __global__ void __launch_bounds__(128, VPL_GATHER_MINB) k_gather(SceneView sv, B
                     }
                     i += gsz;
                 }
-                acc[0] += part[0]; acc[1] += part[1]; acc[2] += part[2];
+                s_acc[0][lane] += part[0]; s_acc[1][lane] += part[1]; s_acc[2][lane] += part[2];
             }
         }
         if (pix >= 0) {
             const float s = (float)(1.0 / kPiR);
             f3 rho = xyz(((const float4*)(gb + pix))[2]);
             float* o = rgb + 3 * (int64_t)pix;
-            o[0] = active ? acc[0] * rho.x * s : 0.0f;
-            o[1] = active ? acc[1] * rho.y * s : 0.0f;
-            o[2] = active ? acc[2] * rho.z * s : 0.0f;
+            o[0] = active ? s_acc[0][lane] * rho.x * s : 0.0f;
+            o[1] = active ? s_acc[1][lane] * rho.y * s : 0.0f;
+            o[2] = active ? s_acc[2][lane] * rho.z * s : 0.0f;
         }
         if (kCount) {
             unsigned long long pairs = active ? (unsigned long long)M : 0ull;
@@ -361,13 +364,13 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
     int dev = 0, sms = 148;
     VPL_CUDA(cudaGetDevice(&dev));
     VPL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    int grid = sms * VPL_GATHER_MINB;  // persistent: VPL_GATHER_MINB CTAs x 4 warps per SM
+    int grid = sms * VPL_GATHER_CTAS;  // persistent: VPL_GATHER_CTAS one-warp CTAs per SM
     SceneView sv = scene_view(d_scene, hh.n);
     BvhView bv = bvh_view(d_bvh, hh.n);
     if (d_ctr)
-        k_gather<true><<<grid, 128, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue);
+        k_gather<true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue);
     else
-        k_gather<false><<<grid, 128, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue);
+        k_gather<false><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue);
     VPL_LAUNCHED("k_gather");
     return VPL_OK;
 }
