@@ -392,7 +392,10 @@ __device__ __forceinline__ int fkey(float f) {   // order-preserving float -> in
 }
 __device__ __forceinline__ float fkey_inv(int k) { return __int_as_float(k ^ ((k >> 31) & 0x7FFFFFFF)); }
 
-constexpr float kConeSpread = 0.1f;  // beam traversal iff max_a (Dmax_a - Dmin_a) < kConeSpread * |D|_min
+#ifndef VPL_CONE_SPREAD
+#define VPL_CONE_SPREAD 0.1f
+#endif
+constexpr float kConeSpread = VPL_CONE_SPREAD;  // beam traversal iff max_a (Dmax_a - Dmin_a) < kConeSpread * |D|_min
 
 // Per-ray packet traversal of the 4-wide BVH: every live lane tests its own
 // ray against the 4 children; a child is entered if any lane's ray enters it.

@@ -33,6 +33,15 @@ namespace vplgi {
 #ifndef VPL_GROUP
 #define VPL_GROUP 1
 #endif
+#ifndef VPL_NO_ORDER
+#define VPL_NO_ORDER 0      // 1: push hit children in lane order (no near-to-far ordering)
+#endif
+#ifndef VPL_CACHE_OWN2
+#define VPL_CACHE_OWN2 1    // test the lane's second most recent occluder
+#endif
+#ifndef VPL_CACHE_WARP
+#define VPL_CACHE_WARP 1    // test the warp's most recent occluder
+#endif
 #ifndef VPL_GROUP_TOL
 #define VPL_GROUP_TOL 0.05f
 #endif
@@ -99,8 +108,8 @@ __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, 
             const float u = dot(s, pv) * inv;
             const float v = dot(d, q) * inv;
             const float t = tq * inv;
-            if ((det != 0.0f) & (u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) & (t > tmin) &
-                (t < S.tmax[k]))
+            // (det == 0 needs no test of its own: u is then NaN or +-inf and fails u >= 0 or u <= 1)
+            if ((u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) & (t > tmin) & (t < S.tmax[k]))
                 hit |= 1u << k;
         }
     }
@@ -212,15 +221,19 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
         unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
         if (Bi) {
             const int nB = __popc(Bi >> 16), nA = __popc(Bi & 0xFFFFu);
-            const int nh = half ? nB : nA;
             const int rank = __popc(Bi & below & hmask);
+#if VPL_NO_ORDER
+            const int pos = (half ? 0 : nB) + rank;
+#else
+            const int nh = half ? nB : nA;
             const bool rev = (dir_neg >> axis) & 1u;   // segments run x -> y along -axis: visit descending
             const int pos = (half ? 0 : nB) + (rev ? rank : nh - 1 - rank);   // first to visit ends on top
+#endif
             if (hit && ref >= 0) sstack[sp + pos] = ref;
             sp += nA + nB;
         }
         __syncwarp();
-        while (Bl) {
+        while (Bl) {   // hit triangle children
             const int k = __ffs(Bl) - 1;
             Bl &= Bl - 1u;
             const int tri = ~__shfl_sync(0xFFFFFFFFu, ref, k) >> 3;
@@ -340,8 +353,8 @@ __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_rec
     if (!__any_sync(0xFFFFFFFFu, traced != 0)) return 0;
     // occluder cache: exact MT against recent occluders
     if (S.pend && cache.own0 >= 0) test_tri<kCount>(bv, x, S, eps, cache.own0, cache, st);
-    if (S.pend && cache.own1 >= 0) test_tri<kCount>(bv, x, S, eps, cache.own1, cache, st);
-    if (S.pend && cache.warp >= 0 && cache.warp != cache.own0 && cache.warp != cache.own1)
+    if (VPL_CACHE_OWN2 && S.pend && cache.own1 >= 0) test_tri<kCount>(bv, x, S, eps, cache.own1, cache, st);
+    if (VPL_CACHE_WARP && S.pend && cache.warp >= 0 && cache.warp != cache.own0 && cache.warp != cache.own1)
         test_tri<kCount>(bv, x, S, eps, cache.warp, cache, st);
     if (kCount) st->chits += __popc(S.occ);
     resolve_group<kCount>(bv, x, S, eps, yk, g, cache, sstack, st);
