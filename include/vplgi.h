@@ -211,6 +211,28 @@ VPL_API int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, cons
                             int32_t tile_w, int32_t tile_h, float* d_rgb, vpl_counters* d_ctr, void* d_work,
                             size_t work_bytes, void* stream);
 
+/* NEXT f2  render_direct: the direct term L_e of Eq. 1 ("L_e(y)
+ * represents direct illumination"; SPEC shade_direct S:327-335; O14,
+ * reading R21) for the listed tiles: per pixel, `samples` uniform points on
+ * every area light drawn from Philox stream 4 (item = pixel index, draws
+ * 2(l*samples+s) and +1), exact fp32 Eq. 2-form irradiance with exact any-hit
+ * visibility, out = rho/pi * E/samples.  d_rgb float[H*W*3]: written
+ * (accumulate = 0) or added to (accumulate = 1, e.g. onto the gather's
+ * indirect image); miss / back-face pixels get 0 (or are left unchanged).
+ * Errors: VPL_EINVAL for null pointers or samples <= 0. */
+VPL_API int32_t vpl_render_direct(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf,
+                          const int32_t* d_tiles, int32_t n_tiles, int32_t tile_w, int32_t tile_h,
+                          int32_t samples, uint64_t seed, int32_t accumulate, float* d_rgb, void* stream);
+
+/* NEXT f1  image_error: the RMSE harness of the paper's equal-sample
+ * comparisons ("RMS" against a > 200k-VPL reference).
+ * d_out double[4] = { sum (img - ref)^2, sum ref^2, sum |img - ref|, sum |ref| }
+ * over n floats (fp64, deterministic order).  d_work: >= 4 * 592 doubles
+ * (18,944 bytes).  d_img / d_ref may be null when n = 0 (all sums 0).
+ * Errors: VPL_EINVAL null / n < 0, VPL_ESMALL short work. */
+VPL_API int32_t vpl_image_error(const float* d_img, const float* d_ref, int64_t n, double* d_out, void* d_work,
+                        size_t work_bytes, void* stream);
+
 /* -------------------------------------------------------------------- */
 /* test hooks: same traversal code as the gather / the walks */
 /* bits per listed pixel: ceil(n_vpls/32) words each of traced and visible */

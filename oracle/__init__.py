@@ -82,6 +82,7 @@ def lib():
             "oracle_gbuffer": (None, [P, P, I64, P]),
             "oracle_gather": (None, [P, P, I64, P, I64, P, P, P, P, P]),
             "oracle_pair_visibility": (None, [P, P, P, I64, P]),
+            "oracle_direct": (None, [P, P, P, I64, C.c_int32, U64, F, P]),
             "oracle_near_strata": (I64, [P, P, P, I64, I64, I64, P]),
             "oracle_walk_range": (None, [P, P, P, I64, I64, P, P]),
             "oracle_abi": (C.c_int, []),
@@ -283,6 +284,18 @@ class OracleScene:
         if bits:
             res["traced_bits"], res["vis_bits"] = tb, vb
         return res
+
+    # ---- O14 (direct term, reading R21) ----
+    def direct(self, gb, pixels, S, seed=None):
+        """Direct radiance at the listed pixels' G-buffer points (gb from
+        gbuffer(pixels)): S uniform light samples per light per pixel."""
+        gb = np.ascontiguousarray(gb, GBUF_DTYPE)
+        pixels = np.ascontiguousarray(pixels, np.int32)
+        rgb = np.zeros((len(gb), 3), np.float32)
+        seed = self.scene.seed if seed is None else seed
+        lib().oracle_direct(self.h, _p(gb), _p(pixels), len(gb), int(S), int(seed), float(np.float32(1.0 / S)),
+                            _p(rgb))
+        return rgb
 
     def pair_visibility(self, x, y):
         x = np.ascontiguousarray(x, np.float32).reshape(-1, 3)

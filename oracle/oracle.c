@@ -74,7 +74,7 @@ uint32_t oracle_draw(uint64_t seed, uint32_t stream, uint32_t item, uint32_t j) 
 /* u32 -> float in [0, 1 - 2^-24], exact */
 static inline float u01(uint32_t x) { return (float)(x >> 8) * 0x1p-24f; }
 
-enum { STREAM_NEAR = 0, STREAM_WALK = 1 };
+enum { STREAM_NEAR = 0, STREAM_WALK = 1, STREAM_DIRECT = 4 };
 
 /* ------------------------------------------------------------------------ */
 /* Scene                                                                     */
@@ -724,6 +724,47 @@ void oracle_gather(const OScene* s, const OGbuf* gb, int64_t n_pix, const OVpl* 
         }
     }
     if (traced_count) *traced_count = total_traced;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O14 — the direct term L_e of Eq. 1 ("L_e(y) represents direct   */
+/* illumination"; SPEC shade_direct S:327-335) for the area lights of BJ:7-11 */
+/* (reading R21): per pixel, S uniform samples y on every light,            */
+/*   E_c += L_l,c * ((A_l * cx) * cl) / (r2 * r2)  if cx > 0, cl > 0, V(x,y), */
+/* d = y - x, cx = n_x.d, cl = -n_l.d (the same form as O8), draws 2(lS+s)  */
+/* and 2(lS+s)+1 of Philox stream 4, item = pixel index; fp32 in this order. */
+/* out_c = (rho_c * (E_c * inv_S)) * INV_PI; miss / back face -> 0.          */
+/* ------------------------------------------------------------------------ */
+void oracle_direct(const OScene* s, const OGbuf* gb, const int32_t* pix, int64_t n_pix, int32_t S, uint64_t seed,
+                   float inv_S, float* rgb) {
+    const float INV_PI = (float)(1.0 / PI_D);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t k = 0; k < n_pix; k++) {
+        const OGbuf* g = gb + k;
+        float E[3] = {0.0f, 0.0f, 0.0f};
+        int ok = g->tri >= 0 && g->front;
+        if (ok) {
+            f3 x = ld3(g->pos), nx = ld3(g->nrm);
+            for (int l = 0; l < s->nL; l++) {
+                const float* L = s->lights + 16 * l;
+                for (int q = 0; q < S; q++) {
+                    uint32_t j = 2u * (uint32_t)(l * S + q);
+                    float u = u01(oracle_draw(seed, STREAM_DIRECT, (uint32_t)pix[k], j));
+                    float v = u01(oracle_draw(seed, STREAM_DIRECT, (uint32_t)pix[k], j + 1));
+                    f3 y = add(add(light_corner(L), scl(u, light_eu(L))), scl(v, light_ev(L)));
+                    f3 d = sub(y, x);
+                    float r2 = dot(d, d);
+                    float cx = dot(nx, d);
+                    float cl = -dot(light_n(L), d);
+                    if (cx > 0.0f && cl > 0.0f && !occluded(s, x, y)) {
+                        float gg = ((L[12] * cx) * cl) / (r2 * r2);
+                        for (int c = 0; c < 3; c++) E[c] += L[13 + c] * gg;
+                    }
+                }
+            }
+        }
+        for (int c = 0; c < 3; c++) rgb[3 * k + c] = ok ? (g->alb[c] * (E[c] * inv_S)) * INV_PI : 0.0f;
+    }
 }
 
 /* visibility of explicit (point, VPL) pairs — for sampled-pair parity */

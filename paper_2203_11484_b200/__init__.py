@@ -23,7 +23,7 @@ FLAG_EMPTY_NEAR, FLAG_EMPTY_FAR, FLAG_WALK_BUDGET_UNMET = 1, 2, 4
 EXPORTS = ["vpl_abi_version", "vpl_status_string", "vpl_last_error", "vpl_launch_count", "vpl_device_info", "vpl_scene_bytes",
            "vpl_scene_upload", "vpl_scene_consts", "vpl_scene_tri_data", "vpl_bvh_bytes", "vpl_build_bvh", "vpl_classify_near_far",
            "vpl_generate_bytes", "vpl_generate_vpls", "vpl_render_gbuffer", "vpl_gather_bytes",
-           "vpl_gather_indirect", "vpl_visibility_dump", "vpl_closest_hit_batch", "vpl_occluded_batch",
+           "vpl_gather_indirect", "vpl_render_direct", "vpl_image_error", "vpl_visibility_dump", "vpl_closest_hit_batch", "vpl_occluded_batch",
            "vpl_philox_batch"]
 
 
@@ -98,6 +98,8 @@ def load_library(path: str | os.PathLike | None = None):
         "vpl_render_gbuffer": (I32, [P, P, P, I32, I32, I32, P, P]),
         "vpl_gather_bytes": (I32, [I32, P]),
         "vpl_gather_indirect": (I32, [P, P, P, P, I32, P, I32, I32, I32, P, P, P, SZ, P]),
+        "vpl_render_direct": (I32, [P, P, P, P, I32, I32, I32, I32, C.c_uint64, I32, P, P]),
+        "vpl_image_error": (I32, [P, P, I64, P, P, SZ, P]),
         "vpl_visibility_dump": (I32, [P, P, P, P, I32, P, I32, P, P, P]),
         "vpl_closest_hit_batch": (I32, [P, P, P, P, I64, F, F, P, P, P]),
         "vpl_occluded_batch": (I32, [P, P, P, P, I64, P, P]),
@@ -280,6 +282,34 @@ def gather_indirect(scene, bvh, gbuf, vpls, tiles, W, H, tw=16, th=16, rgb=None,
                                               tiles.numel(), tw, th, _ptr(rgb), _ptr(ctr), _ptr(work), work.numel(),
                                               _stream(stream)), "vpl_gather_indirect")
     return rgb, ctr
+
+
+def render_direct(scene, bvh, gbuf, tiles, W, H, tw=16, th=16, samples=16, seed=0, rgb=None, accumulate=False,
+                  stream=None):
+    """NEXT f2: direct term L_e of Eq. 1 for the listed tiles (vpl_render_direct)."""
+    dev = scene.device
+    rgb = rgb if rgb is not None else torch.zeros(H * W * 3, dtype=torch.float32, device=dev)
+    _check(load_library().vpl_render_direct(_ptr(scene), _ptr(bvh), _ptr(gbuf), _ptr(tiles), tiles.numel(), tw, th,
+                                            int(samples), int(seed), int(bool(accumulate)), _ptr(rgb),
+                                            _stream(stream)), "vpl_render_direct")
+    return rgb
+
+
+IMAGE_ERROR_WORK_BYTES = 8 * 4 * 592
+
+
+def image_error(img, ref, stream=None) -> dict:
+    """NEXT f1: {rmse, rel_rmse, mae, rel_mae} of img against ref (vpl_image_error)."""
+    assert img.numel() == ref.numel() and img.dtype == torch.float32 and ref.dtype == torch.float32
+    dev = img.device
+    out = torch.zeros(4, dtype=torch.float64, device=dev)
+    work = torch.empty(IMAGE_ERROR_WORK_BYTES, dtype=torch.uint8, device=dev)
+    _check(load_library().vpl_image_error(_ptr(img), _ptr(ref), img.numel(), _ptr(out), _ptr(work), work.numel(),
+                                          _stream(stream)), "vpl_image_error")
+    sq, r2, ad, ar = out.cpu().tolist()
+    n = max(img.numel(), 1)
+    return {"rmse": (sq / n) ** 0.5, "rel_rmse": (sq / r2) ** 0.5 if r2 > 0 else float("nan"),
+            "mae": ad / n, "rel_mae": ad / ar if ar > 0 else float("nan"), "sums": [sq, r2, ad, ar]}
 
 
 def visibility_dump(scene, bvh, gbuf, vpls, pixels, stream=None):

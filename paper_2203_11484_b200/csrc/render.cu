@@ -255,6 +255,84 @@ __global__ void k_vpl_permute(const vpl_record* __restrict__ v, const int32_t* _
     dst[0] = src[0]; dst[1] = src[1]; dst[2] = src[2];
 }
 
+// O14 — direct term L_e of Eq. 1 (reading R21): per pixel, S
+// uniform samples on every area light (Philox stream 4, item = pixel,
+// draws 2(lS+s), 2(lS+s)+1), E_c += L_c ((A cx) cl) / (r2 r2) if visible,
+// out = (rho (E inv_S)) / pi — the same exact-fp32 form as Eq. 2 (O8), so
+// the result is bitwise the oracle's.  One thread per pixel, exact any-hit
+// on the binary BVH.
+__global__ void k_direct(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb, int32_t S,
+                         uint64_t seed, float inv_S, int32_t accumulate, float* __restrict__ rgb) {
+    int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (g >= tm.n_warps()) return;
+    int32_t pix = tm.pixel(g, lane);
+    if (pix < 0) return;
+    const SceneHdr* h = sv.hdr;
+    const float4* gp = (const float4*)(gb + pix);
+    const float4 a = gp[0], b = gp[1], c = gp[2];
+    const bool ok = __float_as_int(a.w) >= 0 && __float_as_int(b.w) != 0;
+    float E[3] = {0.0f, 0.0f, 0.0f};
+    if (ok) {
+        const f3 x = xyz(a), nx = xyz(b);
+        Philox ph(seed, 4u, (uint32_t)pix);
+        for (int l = 0; l < h->nL; ++l) {
+            const float* L = h->lights + 16 * l;
+            const f3 corner = ld3(L), eu = ld3(L + 3), ev = ld3(L + 6), nl = ld3(L + 9);
+            for (int q = 0; q < S; ++q) {
+                const uint32_t j = 2u * (uint32_t)(l * S + q);
+                const float u = u01(ph.at(j)), v = u01(ph.at(j + 1));
+                const f3 y = (corner + u * eu) + v * ev;
+                const f3 d = y - x;
+                const float r2 = dot(d, d);
+                const float cx = dot(nx, d);
+                const float cl = -dot(nl, d);
+                if (cx > 0.0f && cl > 0.0f && !segment_occluded<false>(bv, x, y, h->eps, nullptr)) {
+                    const float gg = ((L[12] * cx) * cl) / (r2 * r2);
+                    E[0] += L[13] * gg; E[1] += L[14] * gg; E[2] += L[15] * gg;
+                }
+            }
+        }
+    }
+    const float INV_PI = (float)(1.0 / kPiR);
+    float* o = rgb + 3 * (int64_t)pix;
+    const float r0 = ok ? (c.x * (E[0] * inv_S)) * INV_PI : 0.0f;
+    const float r1 = ok ? (c.y * (E[1] * inv_S)) * INV_PI : 0.0f;
+    const float r2o = ok ? (c.z * (E[2] * inv_S)) * INV_PI : 0.0f;
+    if (accumulate) { o[0] += r0; o[1] += r1; o[2] += r2o; }
+    else { o[0] = r0; o[1] = r1; o[2] = r2o; }
+}
+
+// NEXT f1 — image error against a reference (the RMSE harness of the
+// paper's equal-sample comparisons): fp64 sums of (a - r)^2, r^2,
+// |a - r|, |r| over n floats.  Deterministic: each block reduces a fixed
+// strided subset in a fixed tree order, one block then adds the partials in
+// block order.
+constexpr int kErrBlocks = 592, kErrThreads = 256;
+__global__ void __launch_bounds__(kErrThreads) k_image_err(const float* __restrict__ a, const float* __restrict__ r,
+                                                           int64_t n, double* __restrict__ part) {
+    __shared__ double sh[4][kErrThreads];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)kErrThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kErrThreads) {
+        const double x = a[i], y = r[i], d = x - y;
+        acc[0] += d * d; acc[1] += y * y; acc[2] += fabs(d); acc[3] += fabs(y);
+    }
+    for (int q = 0; q < 4; ++q) sh[q][threadIdx.x] = acc[q];
+    __syncthreads();
+    for (int w = kErrThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int q = 0; q < 4; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x < 4) part[4 * blockIdx.x + threadIdx.x] = sh[threadIdx.x][0];
+}
+__global__ void k_image_err_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+    if (threadIdx.x >= 4) return;
+    double t = 0.0;
+    for (int b = 0; b < nb; ++b) t += part[4 * b + threadIdx.x];
+    out[threadIdx.x] = t;
+}
+
 struct GatherWork {
     int* queue;
     unsigned* box;
@@ -372,6 +450,42 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
     else
         k_gather<false><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue);
     VPL_LAUNCHED("k_gather");
+    return VPL_OK;
+}
+
+int32_t vpl_render_direct(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf, const int32_t* d_tiles,
+                          int32_t n_tiles, int32_t tile_w, int32_t tile_h, int32_t samples, uint64_t seed,
+                          int32_t accumulate, float* d_rgb, void* stream) {
+    if (!d_scene || !d_bvh || !d_gbuf || !d_rgb || samples <= 0) {
+        set_error("vpl_render_direct: bad arguments");
+        return VPL_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    SceneHdr hh;
+    VPL_TRY(read_scene_hdr(d_scene, s, &hh));
+    TileMap tm;
+    VPL_TRY(make_tilemap(hh, d_tiles, n_tiles, tile_w, tile_h, &tm));
+    if (n_tiles == 0) return VPL_OK;
+    const float inv_S = (float)(1.0 / (double)samples);
+    int64_t threads = tm.n_warps() * 32;
+    k_direct<<<nb(threads, 128), 128, 0, s>>>(scene_view(d_scene, hh.n), bvh_view(d_bvh, hh.n), tm, d_gbuf, samples,
+                                             seed, inv_S, accumulate, d_rgb);
+    VPL_LAUNCHED("k_direct");
+    return VPL_OK;
+}
+
+int32_t vpl_image_error(const float* d_img, const float* d_ref, int64_t n, double* d_out, void* d_work,
+                        size_t work_bytes, void* stream) {
+    if (!d_out || !d_work || n < 0 || (n > 0 && (!d_img || !d_ref))) {
+        set_error("vpl_image_error: bad arguments");
+        return VPL_EINVAL;
+    }
+    if (work_bytes < sizeof(double) * 4 * kErrBlocks) { set_error("vpl_image_error: work too small"); return VPL_ESMALL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    k_image_err<<<kErrBlocks, kErrThreads, 0, s>>>(d_img, d_ref, n, (double*)d_work);
+    VPL_LAUNCHED("k_image_err");
+    k_image_err_final<<<1, 32, 0, s>>>((const double*)d_work, kErrBlocks, d_out);
+    VPL_LAUNCHED("k_image_err_final");
     return VPL_OK;
 }
 

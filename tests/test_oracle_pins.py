@@ -552,3 +552,80 @@ def test_gather_occluder_blocks():
     r = o.gather(g, _vpl([0.0, 2.0, 0.0], nrm=(0, -1, 0)), bits=True)
     assert r["rgb64"][0].max() == 0 and r["rgb64"][1].min() > 0
     assert r["traced_bits"][:, 0].tolist() == [1, 1] and r["vis_bits"][:, 0].tolist() == [0, 1]
+
+
+# ---------------------------------------------------------------- O14 direct term (reading R21)
+def test_direct_irradiance_matches_rectangle_form_factor():
+    """Floor point under the centre of the 0.5 x 0.5 light at H = 1.999: the
+    direct radiance * pi / rho averaged over independent pixels (each with S
+    light samples) equals pi * L * 4 * F_c(0.25/H, 0.25/H) = 0.61286."""
+    s = tiny_scene(floor_quad(2.0))
+    o = oracle.OracleScene(s)
+    n = 4000
+    px = np.arange(n, dtype=np.int32)
+    g = _gb(np.zeros((n, 3), np.float32), rho=0.5)
+    out = o.direct(g, px, 16, seed=9)
+    E = out[:, 0].astype(np.float64) * math.pi / 0.5
+    closed = math.pi * 10.0 * 4 * F_c(0.25 / 1.999, 0.25 / 1.999)
+    m, se = E.mean(), E.std() / math.sqrt(n)
+    assert abs(m - closed) < 4 * se + 1e-5, (m, closed, se)
+    assert np.array_equal(out[:, 0], out[:, 1]) and np.array_equal(out[:, 0], out[:, 2])   # grey light, grey rho
+
+
+def test_direct_tiny_light_hand_value_and_zero_cases():
+    """SPEC shade_direct example for an area light: a light of area A
+    and radiance pi/A at distance 1 straight above, rho = 1 -> 1 (up to the
+    light's size); occluded, behind, back-face and grazing cases give 0."""
+    size = 1e-3
+    L = math.pi / (size * size)
+    light = scenegen.make_light([0.0, 1.0, 0.0], size=size, radiance=(L, L, L))
+    s = tiny_scene(floor_quad(2.0), lights=light)
+    o = oracle.OracleScene(s)
+    g = _gb(np.zeros((4, 3), np.float32), rho=1.0)
+    out = o.direct(g, np.arange(4, dtype=np.int32), 4, seed=3)
+    assert np.allclose(out, 1.0, rtol=1e-5), out
+    g2 = g.copy()
+    g2["nrm"] = [0, -1, 0]                                    # receiver faces away from the light
+    assert o.direct(g2, np.arange(4, dtype=np.int32), 4).max() == 0
+    g3 = g.copy()
+    g3["front"] = 0                                           # back face
+    assert o.direct(g3, np.arange(4, dtype=np.int32), 4).max() == 0
+    g4 = g.copy()
+    g4["pos"] = [[0.0, 1.0, 3.0]] * 4                         # light exactly edge-on (cl = 0, cx = 0)
+    g4["nrm"] = [0, 0, 1]
+    assert o.direct(g4, np.arange(4, dtype=np.int32), 4).max() == 0
+    blk = np.concatenate([floor_quad(2.0), scenegen.quad_tris([-1, 0.5, -1], [2, 0, 0], [0, 0, 2])])
+    ob = oracle.OracleScene(tiny_scene(blk, lights=light))
+    assert ob.direct(g, np.arange(4, dtype=np.int32), 4).max() == 0   # blocker between
+
+
+def test_direct_linear_in_radiance_and_sample_mean():
+    """Doubling the light radiance doubles the output bitwise (every term
+    scales by 2); with S samples the output is the mean of the S single-
+    sample estimates drawn from the same counter slots (draws 2(lS+s), +1)."""
+    s1 = tiny_scene(floor_quad(2.0))
+    l2 = scenegen.make_light([0.0, 1.999, 0.0], radiance=(20.0, 20.0, 20.0))
+    s2 = tiny_scene(floor_quad(2.0), lights=l2)
+    g = _gb(np.array([[0.3, 0, -0.2], [1.2, 0, 0.7]], np.float32), rho=0.5)
+    px = np.array([5, 77], np.int32)
+    a = oracle.OracleScene(s1).direct(g, px, 8, seed=2)
+    b = oracle.OracleScene(s2).direct(g, px, 8, seed=2)
+    assert np.array_equal(2 * a, b)
+    # S = 2 from S = 1 estimates: sample 1 uses draws (2, 3), i.e. the S=1 estimate of a pixel whose
+    # draws are shifted by one sample -- checked through the float64 re-evaluation of the same samples
+    o = oracle.OracleScene(s1)
+    one = o.direct(g, px, 2, seed=2).astype(np.float64)
+    Lt = s1.lights.reshape(-1, 16)[0]
+    ref = []
+    for k, p in enumerate(px):
+        x = g["pos"][k].astype(np.float64)
+        E = 0.0
+        for q in range(2):
+            u = (oracle.draw(2, 4, int(p), 2 * q) >> 8) * 2.0 ** -24
+            v = (oracle.draw(2, 4, int(p), 2 * q + 1) >> 8) * 2.0 ** -24
+            y = Lt[0:3] + u * Lt[3:6] + v * Lt[6:9]
+            d = y - x
+            r2 = d @ d
+            E += 10.0 * Lt[12] * d[1] * d[1] / (r2 * r2)
+        ref.append(0.5 * E / 2 / math.pi)
+    assert np.allclose(one[:, 0], ref, rtol=1e-5)
