@@ -233,6 +233,29 @@ VPL_API int32_t vpl_render_direct(const void* d_scene, const void* d_bvh, const 
 VPL_API int32_t vpl_image_error(const float* d_img, const float* d_ref, int64_t n, double* d_out, void* d_work,
                         size_t work_bytes, void* stream);
 
+/* NEXT f3  generate_rejection: the rejection-sampling comparator (P:29-32
+ * [r3], "reject those VPLs that contribute less than the average value to
+ * the resulting image"; O15, reading R23).
+ * d_pilot: n_pilot candidate records (plain IR: vpl_generate_vpls with every
+ * patch FAR).  64 probe pixels (8 x 8 blocks, offsets from Philox stream 5,
+ * item = block) get their G-buffer points (O12); candidate i scores
+ * s_i = sum over probes, in order, of its Eq. 1 summand as luminance (exact
+ * fp32, exact visibility); mean = fp64 sum / n_pilot;
+ * p_i = max(0.05, min(1, s_i / mean)); i is accepted iff
+ * U(Philox stream 6, item i, draw 0) < p_i, scanning in index order until
+ * `budget` are accepted (scanned = index of the last + 1, else n_pilot);
+ * kept flux *= (float)((n_pilot / scanned) / p_i).  Outputs: d_out (up to
+ * min(budget, n_pilot) records, the accepted ones in index order),
+ * d_accepted int64 (their number); nullable: d_scores float[n_pilot],
+ * d_mean double, d_scanned int64, d_probe_pixels int32[64].  d_work:
+ * vpl_rejection_bytes(n_pilot) bytes.  Errors: VPL_EINVAL (null, n_pilot <= 0
+ * or > 2^31 - 1, budget <= 0), VPL_ESMALL (short work). */
+VPL_API int32_t vpl_rejection_bytes(int64_t n_pilot, size_t* work_bytes);
+VPL_API int32_t vpl_generate_rejection(const void* d_scene, const void* d_bvh, const vpl_record* d_pilot,
+                               int64_t n_pilot, int64_t budget, uint64_t seed, vpl_record* d_out,
+                               float* d_scores, double* d_mean, int64_t* d_accepted, int64_t* d_scanned,
+                               int32_t* d_probe_pixels, void* d_work, size_t work_bytes, void* stream);
+
 /* -------------------------------------------------------------------- */
 /* test hooks: same traversal code as the gather / the walks */
 /* bits per listed pixel: ceil(n_vpls/32) words each of traced and visible */

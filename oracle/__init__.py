@@ -83,6 +83,8 @@ def lib():
             "oracle_gather": (None, [P, P, I64, P, I64, P, P, P, P, P]),
             "oracle_pair_visibility": (None, [P, P, P, I64, P]),
             "oracle_direct": (None, [P, P, P, I64, C.c_int32, U64, F, P]),
+            "oracle_probe_pixels": (None, [C.c_int, C.c_int, U64, P]),
+            "oracle_rejection": (I64, [P, P, I64, P, I64, I64, U64, P, P, P, P]),
             "oracle_near_strata": (I64, [P, P, P, I64, I64, I64, P]),
             "oracle_walk_range": (None, [P, P, P, I64, I64, P, P]),
             "oracle_abi": (C.c_int, []),
@@ -296,6 +298,36 @@ class OracleScene:
         lib().oracle_direct(self.h, _p(gb), _p(pixels), len(gb), int(S), int(seed), float(np.float32(1.0 / S)),
                             _p(rgb))
         return rgb
+
+    # ---- O15 (rejection-sampling comparator, reading R23) ----
+    def probe_pixels(self, seed=None):
+        out = np.zeros(64, np.int32)
+        s = self.scene
+        lib().oracle_probe_pixels(s.width, s.height, int(s.seed if seed is None else seed), _p(out))
+        return out
+
+    def rejection(self, pilot, budget, seed=None, gb=None):
+        """Keep up to `budget` of the pilot VPLs by the probe-score rejection
+        rule (O15).  gb: explicit probe G-buffer records (default: the 64 probe
+        pixels' G-buffer; probes and acceptance draws use `seed`, default the
+        scene seed).  Returns (vpls, info {accepted, mean, scores, n_scanned,
+        probes})."""
+        pilot = np.ascontiguousarray(pilot, VPL_DTYPE)
+        seed = self.scene.seed if seed is None else seed
+        px = None
+        if gb is None:
+            px = self.probe_pixels(seed)
+            gb = self.gbuffer(px)
+        gb = np.ascontiguousarray(gb, GBUF_DTYPE)
+        B = min(int(budget), len(pilot))
+        out = np.zeros(max(B, 1), VPL_DTYPE)
+        sc = np.zeros(max(len(pilot), 1), np.float32)
+        mean = C.c_double()
+        scanned = C.c_int64()
+        acc = lib().oracle_rejection(self.h, _p(gb), len(gb), _p(pilot), len(pilot), int(budget), int(seed), _p(out),
+                                     _p(sc), C.byref(mean), C.byref(scanned))
+        return out[:acc], dict(accepted=int(acc), mean=float(mean.value), scores=sc[:len(pilot)],
+                               n_scanned=int(scanned.value), probes=px)
 
     def pair_visibility(self, x, y):
         x = np.ascontiguousarray(x, np.float32).reshape(-1, 3)

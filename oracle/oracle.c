@@ -74,7 +74,7 @@ uint32_t oracle_draw(uint64_t seed, uint32_t stream, uint32_t item, uint32_t j) 
 /* u32 -> float in [0, 1 - 2^-24], exact */
 static inline float u01(uint32_t x) { return (float)(x >> 8) * 0x1p-24f; }
 
-enum { STREAM_NEAR = 0, STREAM_WALK = 1, STREAM_DIRECT = 4 };
+enum { STREAM_NEAR = 0, STREAM_WALK = 1, STREAM_DIRECT = 4, STREAM_PROBE = 5, STREAM_REJECT = 6 };
 
 /* ------------------------------------------------------------------------ */
 /* Scene                                                                     */
@@ -765,6 +765,98 @@ void oracle_direct(const OScene* s, const OGbuf* gb, const int32_t* pix, int64_t
         }
         for (int c = 0; c < 3; c++) rgb[3 * k + c] = ok ? (g->alb[c] * (E[c] * inv_S)) * INV_PI : 0.0f;
     }
+}
+
+/* ------------------------------------------------------------------------ */
+/* O15 — the rejection-sampling comparator (P:29-32 [r3]: "reject those VPLs */
+/* that contribute less than the average value to the resulting image";     */
+/* SPEC generate_rejection_vpls S:252-260; reading R23).                     */
+/* Probes: a 8 x 8 grid of image blocks, one pixel per block, offset        */
+/* floor(U(draw 0 / 1 of Philox stream 5, item b) * block size).             */
+/* ------------------------------------------------------------------------ */
+void oracle_probe_pixels(int W, int H, uint64_t seed, int32_t* pix /* [64] */) {
+    for (int b = 0; b < 64; b++) {
+        int bx = b % 8, by = b / 8;
+        int x0 = bx * W / 8, x1 = (bx + 1) * W / 8, y0 = by * H / 8, y1 = (by + 1) * H / 8;
+        float u = u01(oracle_draw(seed, STREAM_PROBE, (uint32_t)b, 0));
+        float v = u01(oracle_draw(seed, STREAM_PROBE, (uint32_t)b, 1));
+        int px = x0 + (int)(u * (float)(x1 - x0));
+        int py = y0 + (int)(v * (float)(y1 - y0));
+        pix[b] = py * W + px;
+    }
+}
+
+/* lum(c) = ((c.r + c.g) + c.b) / 3 */
+static inline float lum3(const float* c) { return ((c[0] + c[1]) + c[2]) / 3.0f; }
+
+/* Score of candidate i: s_i = sum over probes q = 0..nq-1, in that order, in
+ * fp32 of t_iq = ((cx*ci) / (r2 * max(r2, b^2)) * lum(Phi_i)) * lum(rho_q)
+ * when the Eq. 1 term is traced (O13's cull and self-exclusion) and visible,
+ * else 0 — the Eq. 1 summand of the VPL at the probe, as luminance.
+ * mean = fp64 sum of the scores in index order / pilot.
+ * Acceptance ([r3]'s rejection rule, made unbiased — reading R23):
+ *   p_i = max(P_MIN, min(1, s_i / mean)) in fp64 (p_i = 1 when mean = 0),
+ *   accept iff (double)U(draw 0 of Philox stream 6, item i) < p_i,
+ * scanning in index order until `budget` are accepted (n_scanned = index of
+ * the last one + 1, or pilot).  Kept flux = Phi * (float)((pilot / n_scanned)
+ * / p_i): the scanned prefix stands for the whole pilot, 1/p_i undoes the
+ * thinning.  Returns the number accepted (<= budget); out holds them. */
+#define REJ_P_MIN 0.05
+int64_t oracle_rejection(const OScene* s, const OGbuf* probes, int64_t nq, const OVpl* pilot, int64_t np_,
+                         int64_t budget, uint64_t seed, OVpl* out, float* scores, double* mean_out,
+                         int64_t* n_scanned_out) {
+    float* sc = scores ? scores : (float*)malloc(sizeof(float) * (size_t)(np_ > 0 ? np_ : 1));
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t i = 0; i < np_; i++) {
+        float acc = 0.0f;
+        float li = lum3(pilot[i].flux);
+        f3 y = ld3(pilot[i].pos), ny = ld3(pilot[i].nrm);
+        for (int64_t q = 0; q < nq; q++) {
+            const OGbuf* g = probes + q;
+            float t = 0.0f;
+            if (g->tri >= 0 && g->front && g->tri != pilot[i].tri) {
+                f3 x = ld3(g->pos), nx = ld3(g->nrm);
+                f3 d = sub(y, x);
+                float r2 = dot(d, d);
+                float cx = dot(nx, d);
+                float ci = -dot(ny, d);
+                if (cx > 0.0f && ci > 0.0f && !occluded(s, x, y)) {
+                    float w = (cx * ci) / (r2 * (r2 > s->b2 ? r2 : s->b2));
+                    t = (w * li) * lum3(g->alb);
+                }
+            }
+            acc += t;
+        }
+        sc[i] = acc;
+    }
+    double sum = 0.0;
+    for (int64_t i = 0; i < np_; i++) sum += (double)sc[i];
+    double mean = np_ > 0 ? sum / (double)np_ : 0.0;
+    if (mean_out) *mean_out = mean;
+    int64_t* acc_i = (int64_t*)malloc(sizeof(int64_t) * (size_t)(budget > 0 ? budget : 1));
+    double* acc_p = (double*)malloc(sizeof(double) * (size_t)(budget > 0 ? budget : 1));
+    int64_t o = 0, scanned = np_;
+    for (int64_t i = 0; i < np_ && o < budget; i++) {
+        double p = mean > 0.0 ? (double)sc[i] / mean : 1.0;
+        if (p > 1.0) p = 1.0;
+        if (p < REJ_P_MIN) p = REJ_P_MIN;
+        double u = (double)u01(oracle_draw(seed, STREAM_REJECT, (uint32_t)i, 0));
+        if (u < p) {
+            acc_i[o] = i;
+            acc_p[o] = p;
+            o++;
+            if (o == budget) scanned = i + 1;
+        }
+    }
+    for (int64_t k = 0; k < o; k++) {
+        float f = (float)(((double)np_ / (double)scanned) / acc_p[k]);
+        out[k] = pilot[acc_i[k]];
+        for (int c = 0; c < 3; c++) out[k].flux[c] = out[k].flux[c] * f;
+    }
+    free(acc_i); free(acc_p);
+    if (!scores) free(sc);
+    if (n_scanned_out) *n_scanned_out = scanned;
+    return o;
 }
 
 /* visibility of explicit (point, VPL) pairs — for sampled-pair parity */

@@ -23,7 +23,8 @@ FLAG_EMPTY_NEAR, FLAG_EMPTY_FAR, FLAG_WALK_BUDGET_UNMET = 1, 2, 4
 EXPORTS = ["vpl_abi_version", "vpl_status_string", "vpl_last_error", "vpl_launch_count", "vpl_device_info", "vpl_scene_bytes",
            "vpl_scene_upload", "vpl_scene_consts", "vpl_scene_tri_data", "vpl_bvh_bytes", "vpl_build_bvh", "vpl_classify_near_far",
            "vpl_generate_bytes", "vpl_generate_vpls", "vpl_render_gbuffer", "vpl_gather_bytes",
-           "vpl_gather_indirect", "vpl_render_direct", "vpl_image_error", "vpl_visibility_dump", "vpl_closest_hit_batch", "vpl_occluded_batch",
+           "vpl_gather_indirect", "vpl_render_direct", "vpl_image_error", "vpl_rejection_bytes",
+           "vpl_generate_rejection", "vpl_visibility_dump", "vpl_closest_hit_batch", "vpl_occluded_batch",
            "vpl_philox_batch"]
 
 
@@ -100,6 +101,8 @@ def load_library(path: str | os.PathLike | None = None):
         "vpl_gather_indirect": (I32, [P, P, P, P, I32, P, I32, I32, I32, P, P, P, SZ, P]),
         "vpl_render_direct": (I32, [P, P, P, P, I32, I32, I32, I32, C.c_uint64, I32, P, P]),
         "vpl_image_error": (I32, [P, P, I64, P, P, SZ, P]),
+        "vpl_rejection_bytes": (I32, [I64, P]),
+        "vpl_generate_rejection": (I32, [P, P, P, I64, I64, C.c_uint64, P, P, P, P, P, P, P, SZ, P]),
         "vpl_visibility_dump": (I32, [P, P, P, P, I32, P, I32, P, P, P]),
         "vpl_closest_hit_batch": (I32, [P, P, P, P, I64, F, F, P, P, P]),
         "vpl_occluded_batch": (I32, [P, P, P, P, I64, P, P]),
@@ -293,6 +296,33 @@ def render_direct(scene, bvh, gbuf, tiles, W, H, tw=16, th=16, samples=16, seed=
                                             int(samples), int(seed), int(bool(accumulate)), _ptr(rgb),
                                             _stream(stream)), "vpl_render_direct")
     return rgb
+
+
+def generate_rejection(scene, bvh, pilot, budget, seed, stream=None):
+    """NEXT f3: keep up to `budget` pilot VPLs by the probe-score rejection rule
+    (vpl_generate_rejection).  Returns (vpls uint8 [n, 48], info {accepted,
+    mean, scores, n_scanned, probes}).  Synchronises."""
+    dev = scene.device
+    pilot = pilot.contiguous().view(-1, VPL_RECORD_BYTES)
+    n = pilot.shape[0]
+    B = min(int(budget), n)
+    wb = C.c_size_t()
+    _check(load_library().vpl_rejection_bytes(n, C.byref(wb)), "vpl_rejection_bytes")
+    work = torch.empty(max(wb.value, 1), dtype=torch.uint8, device=dev)
+    out = torch.empty(max(B, 1) * VPL_RECORD_BYTES, dtype=torch.uint8, device=dev)
+    scores = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    mean = torch.zeros(1, dtype=torch.float64, device=dev)
+    acc = torch.zeros(1, dtype=torch.int64, device=dev)
+    scanned = torch.zeros(1, dtype=torch.int64, device=dev)
+    probes = torch.zeros(64, dtype=torch.int32, device=dev)
+    _check(load_library().vpl_generate_rejection(_ptr(scene), _ptr(bvh), _ptr(pilot), n, int(budget), int(seed),
+                                                 _ptr(out), _ptr(scores), _ptr(mean), _ptr(acc), _ptr(scanned),
+                                                 _ptr(probes), _ptr(work), work.numel(), _stream(stream)),
+           "vpl_generate_rejection")
+    torch.cuda.synchronize(dev)
+    a = int(acc.item())
+    return out[: a * VPL_RECORD_BYTES].view(-1, VPL_RECORD_BYTES), dict(
+        accepted=a, mean=float(mean.item()), scores=scores[:n], n_scanned=int(scanned.item()), probes=probes)
 
 
 IMAGE_ERROR_WORK_BYTES = 8 * 4 * 592

@@ -14,7 +14,7 @@ LIB = PKG / "libvplgi.so"
 OBJ = PKG / "build"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["api.cu", "scene.cu", "bvh.cu", "generate.cu", "render.cu"]
+SOURCES = ["api.cu", "scene.cu", "bvh.cu", "generate.cu", "render.cu", "reject.cu"]
 # -fmad=false: the bit-exact steps (DESIGN.md §3 O0) must not contract a*b+c;
 # kernels that want FMA call fmaf() explicitly.
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-fmad=false",

@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import torch
 
-from . import (Renderer, all_tiles, classify_near_far, gather_indirect, generate_vpls, image_error)
+from . import (Renderer, all_tiles, gather_indirect, generate_rejection, generate_vpls, image_error)
 
 
 def _timed(fn):
@@ -23,9 +23,11 @@ def _timed(fn):
     return out, e0.elapsed_time(e1)
 
 
-def compare_estimators(scene, M_list=(1024, 4096), ref_M=262144, ref_seed=None, device="cuda", return_images=False):
+def compare_estimators(scene, M_list=(1024, 4096), ref_M=262144, ref_seed=None, device="cuda", return_images=False,
+                       pilot_factor=4):
     """Returns {"ref": {...}, "ref_hybrid": {...}, "runs": [{"M", "hybrid",
-    "hybrid_vs_own", "ir"}]}.  Hybrid: near fraction K_near/M of the scene's
+    "hybrid_vs_own", "ir", "rejection"}]}.  Rejection (f3, O15): an IR pilot of
+    pilot_factor * M candidates scored at 64 probe pixels, M kept.  Hybrid: near fraction K_near/M of the scene's
     own configuration; IR: all patches FAR (K = 0, M_far = M, budget rule O10).
     References (independent seed ref_seed, default scene.seed + 1000): dense
     IR with ref_M VPLs (the paper's reference) and the dense hybrid with
@@ -63,14 +65,21 @@ def compare_estimators(scene, M_list=(1024, 4096), ref_M=262144, ref_seed=None, 
         K = int(frac * M + 0.5)
         h_img, h_info, hg, ht = render(r.labels, M, K, s.seed)
         i_img, i_info, ig, it = render(far, M, 0, s.seed)
+        # rejection comparator (f3): IR pilot of pilot_factor * M candidates, keep M by probe score
+        (pv, p_info, _), pg = _timed(lambda: generate_vpls(r.scene, r.bvh, far, r.n, pilot_factor * M, 0,
+                                                           s.max_depth, s.rr, s.seed, max_out=pilot_factor * M))
+        (rv, r_info), rg = _timed(lambda: generate_rejection(r.scene, r.bvh, pv, M, s.seed))
+        (j_img, _), jt = _timed(lambda: gather_indirect(r.scene, r.bvh, r.gbuf, rv, tiles, W, H, 16, 16))
         if return_images:
-            images[M] = (h_img.clone(), i_img.clone())
+            images[M] = (h_img.clone(), i_img.clone(), j_img.clone())
         out["runs"].append({
             "M": M,
             "hybrid": dict(image_error(h_img, ref_img), K=h_info["K"], M_far=h_info["M_far"], gen_ms=hg,
                            gather_ms=ht),
             "hybrid_vs_own": image_error(h_img, refh_img),
             "ir": dict(image_error(i_img, ref_img), K=i_info["K"], M_far=i_info["M_far"], gen_ms=ig, gather_ms=it),
+            "rejection": dict(image_error(j_img, ref_img), pilot=pilot_factor * M, accepted=r_info["accepted"],
+                              n_scanned=r_info["n_scanned"], gen_ms=pg + rg, gather_ms=jt),
         })
     if return_images:
         images["ref"] = ref_img

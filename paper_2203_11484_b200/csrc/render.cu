@@ -15,35 +15,7 @@ __global__ void k_gbuffer(SceneView sv, BvhView bv, TileMap tm, vpl_gpoint* __re
     if (g >= tm.n_warps()) return;
     int32_t pix = tm.pixel(g, lane);
     if (pix < 0) return;
-    const SceneHdr* h = sv.hdr;
-    const float* c = h->cam;
-    int px = pix % h->W, py = pix / h->W;
-    f3 pos = ld3(c), fwd = ld3(c + 3), up = ld3(c + 6), right = ld3(c + 9);
-    float sx = ((2.0f * ((float)px + 0.5f)) / (float)h->W - 1.0f) * c[12];
-    float sy = (1.0f - (2.0f * ((float)py + 0.5f)) / (float)h->H) * c[13];
-    f3 d = (fwd + sx * right) + sy * up;
-    float len = sqrtf(dot(d, d));
-    f3 dir = mk3(d.x / len, d.y / len, d.z / len);
-    Ray r = make_ray(pos, dir, 0.0f, __int_as_float(0x7f800000));
-    float t;
-    int hit = bvh_closest(bv, r, t);
-    vpl_gpoint o;
-    if (hit < 0) {
-        o.pos[0] = o.pos[1] = o.pos[2] = 0.0f;
-        o.nrm[0] = o.nrm[1] = o.nrm[2] = 0.0f;
-        o.alb[0] = o.alb[1] = o.alb[2] = 0.0f;
-        o.tri = -1; o.front = 0; o.t = 0.0f;
-    } else {
-        f3 x = pos + t * dir;
-        float4 n = sv.nrm[hit];
-        float4 a = sv.alb[hit];
-        o.pos[0] = x.x; o.pos[1] = x.y; o.pos[2] = x.z;
-        o.nrm[0] = n.x; o.nrm[1] = n.y; o.nrm[2] = n.z;
-        o.alb[0] = a.x; o.alb[1] = a.y; o.alb[2] = a.z;
-        o.tri = hit; o.t = t;
-        o.front = dot(xyz(n), dir) < 0.0f;
-    }
-    gb[pix] = o;
+    gb[pix] = primary_hit(sv, bv, pix);
 }
 
 // a8 — Eq. 1 gather.  Persistent: each warp takes 8x4 pixel blocks

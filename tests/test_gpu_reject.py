@@ -1,0 +1,41 @@
+"""GPU parity of NEXT row f3 — the rejection-sampling comparator (
+DESIGN.md O15, reading R23) — against the oracle: probe pixels, per-candidate
+scores, mean and the kept / filled VPL set must all be bitwise equal."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2203_11484_b200 as V
+import scenegen
+from gpu_helpers import GpuScene, assert_vpls_bitwise, vpls_to_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cfg,pilot,budget", [(1, 1024, 256), (1, 1024, 1024), (2, 4096, 1024), (3, 2048, 512)])
+def test_rejection_bitwise(cfg, pilot, budget):
+    s = scenegen.make_scene(cfg)
+    gs, os_ = GpuScene(s), oracle.OracleScene(s)
+    lab = np.zeros(s.n_tris, np.uint8)
+    pv, info = gs.generate(labels=lab, M=pilot, K_near=0)
+    out, ri = V.generate_rejection(gs.scene, gs.bvh, pv, budget, seed=s.seed)
+    opv = vpls_to_oracle(V.decode_vpls(pv))
+    oo, oi = os_.rejection(opv, budget, seed=s.seed)
+    assert np.array_equal(ri["probes"].cpu().numpy(), oi["probes"])
+    sc = ri["scores"].cpu().numpy()
+    assert np.array_equal(sc.view(np.uint32), oi["scores"].view(np.uint32))
+    assert ri["mean"] == oi["mean"] and ri["accepted"] == oi["accepted"] and ri["n_scanned"] == oi["n_scanned"]
+    assert_vpls_bitwise(V.decode_vpls(out), oo)
+    assert (sc > 0).any()
+
+
+def test_rejection_budget_above_pilot_and_bad_args():
+    s = scenegen.make_scene(1)
+    gs = GpuScene(s)
+    pv, _ = gs.generate(labels=np.zeros(s.n_tris, np.uint8), M=64, K_near=0)
+    out, ri = V.generate_rejection(gs.scene, gs.bvh, pv, 100, seed=1)
+    assert out.shape[0] == ri["accepted"] <= 64 and ri["n_scanned"] == 64   # budget above the pilot: all scanned
+    with pytest.raises(V.VplError):
+        V.generate_rejection(gs.scene, gs.bvh, pv, 0, seed=1)

@@ -629,3 +629,77 @@ def test_direct_linear_in_radiance_and_sample_mean():
             E += 10.0 * Lt[12] * d[1] * d[1] / (r2 * r2)
         ref.append(0.5 * E / 2 / math.pi)
     assert np.allclose(one[:, 0], ref, rtol=1e-5)
+
+
+# ---------------------------------------------------------------- O15 rejection comparator (reading R23)
+def test_rejection_probe_pixels_one_per_block():
+    s = scenegen.make_scene(1)
+    o = oracle.OracleScene(s)
+    for W, H in ((64, 64), (37, 23), (1920, 1080)):
+        s2 = scenegen.custom_scene(s.verts, s.albedo, s.lights, s.cam, W, H)
+        px = oracle.OracleScene(s2).probe_pixels(seed=4)
+        x, y = px % W, px // W
+        bx, by = np.arange(64) % 8, np.arange(64) // 8
+        assert np.all((x >= bx * W // 8) & (x < (bx + 1) * W // 8))
+        assert np.all((y >= by * H // 8) & (y < (by + 1) * H // 8))
+    assert not np.array_equal(o.probe_pixels(seed=1), o.probe_pixels(seed=2))
+
+
+def test_rejection_score_hand_value_and_dominance():
+    """One probe under three VPLs: a facing VPL at height h scores
+    (1/h^2) lum(Phi) lum(rho) (cx = ci = h, r2 = h^2 > b^2); a VPL facing away
+    and one behind the probe score 0.  The facing one has p = 1 and is always
+    kept; with every candidate scanned its flux keeps its scale (pilot/scanned
+    = 1, 1/p = 1)."""
+    s, o = _gather_setup()
+    h = 3.0
+    g = _gb(np.zeros((1, 3), np.float32), rho=0.8)
+    g["alb"] = [0.2, 0.4, 0.6]
+    pv = np.concatenate([_vpl([0.0, -1.0, 0.0], nrm=(0, 1, 0)),           # behind the probe
+                         _vpl([0.5, h, 0.0], nrm=(0, 1, 0)),               # faces away
+                         _vpl([0.0, h, 0.0], flux=(1.0, 2.0, 6.0))])       # facing, straight above
+    pv["walk"] = [0, 1, 2]
+    expect = (1.0 / (h * h)) * 3.0 * (((0.2 + 0.4) + 0.6) / 3.0)
+    for seed in range(20):
+        out, info = o.rejection(pv, 3, seed=seed, gb=g)
+        assert info["scores"][0] == 0 and info["scores"][1] == 0
+        assert abs(info["scores"][2] - expect) < 1e-6 * expect
+        assert info["n_scanned"] == 3 and out["walk"][-1] == 2
+        assert out["flux"][-1].tolist() == [1.0, 2.0, 6.0]
+        if len(out) > 1:                                                  # a p = 0.05 candidate got in
+            assert np.allclose(out["flux"][0], pv["flux"][out["walk"][0]] * 20.0, rtol=1e-6)
+
+
+def test_rejection_ties_keep_generation_order():
+    """Identical candidates: every p is 1, so the first `budget` are kept in
+    order, the scanned prefix is `budget` long and fluxes scale by pilot/budget."""
+    s, o = _gather_setup()
+    g = _gb(np.array([[0.0, 0, 0], [1.0, 0, 0.5]], np.float32))
+    pv = np.concatenate([_vpl([0.2, 2.0, 0.1])] * 10)
+    pv["walk"] = np.arange(10)
+    out, info = o.rejection(pv, 4, seed=1, gb=g)
+    assert info["accepted"] == 4 and info["n_scanned"] == 4 and out["walk"].tolist() == [0, 1, 2, 3]
+    assert np.array_equal(out["flux"], pv["flux"][:4] * np.float32(2.5))
+
+
+def test_rejection_is_unbiased_in_power():
+    """With the whole pilot scanned, E[sum of kept flux] = sum of pilot flux
+    (each candidate kept with probability p_i, weighted 1/p_i): the mean over
+    400 acceptance seeds (fixed probes) agrees within 4 sigma; the accepted
+    count averages sum_i p_i."""
+    s1 = scenegen.make_scene(1)
+    o1 = oracle.OracleScene(s1)
+    pilot, _ = o1.generate_vpls(np.zeros(s1.n_tris, np.uint8), M=512, K_near=0)
+    gb = o1.gbuffer(o1.probe_pixels(seed=1))
+    tot = pilot["flux"][:, 0].astype(np.float64).sum()
+    sums, counts = [], []
+    for seed in range(400):
+        out, info = o1.rejection(pilot, len(pilot), seed=seed, gb=gb)
+        sums.append(out["flux"][:, 0].astype(np.float64).sum())
+        counts.append(info["accepted"])
+    sc = info["scores"].astype(np.float64)
+    p = np.clip(sc / info["mean"], 0.05, 1.0)
+    m, se = np.mean(sums), np.std(sums) / math.sqrt(len(sums))
+    assert abs(m - tot) < 4 * se + 1e-6 * tot, (m, tot, se)
+    assert abs(np.mean(counts) - p.sum()) < 4 * np.std(counts) / math.sqrt(len(counts)) + 1e-9
+    assert info["n_scanned"] == len(pilot)
