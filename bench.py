@@ -272,7 +272,8 @@ def run_ours(args):
             "counters": dict(c, tri_tests_per_traced=c["tri_tests"] / max(traced, 1),
                              steps_per_packet=c["warp_steps"] / max(c["warp_rays"], 1),
                              cone_packet_fraction=c["cone_packets"] / max(c["warp_rays"], 1),
-                             cache_hit_fraction=c["cache_hits"] / max(traced, 1)),
+                             cache_hit_fraction=c["cache_hits"] / max(traced, 1),
+                             cache_tests_per_traced=c["cache_tests"] / max(traced, 1)),
             "roofline": {"bound": "alu", "kernel": "k_gather", "achieved": achieved / 1e12,
                          "peak": peak_ops / 1e12, "unit": "Tops/s", "frac": achieved / peak_ops,
                          "traffic": None,

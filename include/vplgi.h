@@ -127,6 +127,7 @@ typedef struct {
     unsigned long long cone_packets; /* packets traversed with the cone test */
     unsigned long long ray_packets;  /* packets traversed with per-ray tests (loose cones) */
     unsigned long long cache_hits;   /* traced lanes resolved by the occluder cache */
+    unsigned long long cache_tests;  /* exact MT tests spent in the occluder cache (part of tri_tests) */
 } vpl_counters;
 
 /* -------------------------------------------------------------------- */

@@ -52,7 +52,7 @@ class vpl_gen_info(C.Structure):
 
 
 COUNTER_NAMES = ["pairs", "traced", "visible", "box_tests", "tri_tests", "warp_rays", "warp_steps", "cone_tests",
-                 "cone_packets", "ray_packets", "cache_hits"]
+                 "cone_packets", "ray_packets", "cache_hits", "cache_tests"]
 
 
 class vpl_counters(C.Structure):

@@ -253,6 +253,7 @@ struct TravStats {
     uint32_t boxes = 0, tris = 0;
     uint32_t wrays = 0, wsteps = 0;  // warp-level packets / iterations (counted on lane 0)
     uint32_t cones = 0, cpk = 0, rpk = 0, chits = 0;  // cone tests, cone / per-ray packets, cache hits
+    uint32_t ctests = 0;                              // MT tests in the occluder cache
 };
 
 // leaf refs: ~((first << 3) | (count - 1)), count in [1, 8]
@@ -381,6 +382,7 @@ __device__ __forceinline__ bool segment_occluded(const BvhView& bv, f3 a, f3 b, 
 struct OccluderCache {
     int own0 = -1, own1 = -1;  // this lane's two most recent occluders (leaf-order triangle index)
     int warp = -1;             // the warp's most recent occluder (uniform)
+    bool vis_streak = false;   // last traced segment of this lane was visible (VPL_CACHE_STREAK)
     __device__ __forceinline__ void found(int tri) {
         if (tri != own0) { own1 = own0; own0 = tri; }
     }

@@ -98,10 +98,10 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
         }
         if (kCount) {
             unsigned long long pairs = active ? (unsigned long long)M : 0ull;
-            unsigned long long v[11] = {pairs, n_traced, n_vis, st.boxes, st.tris, st.wrays, st.wsteps,
-                                        st.cones, st.cpk, st.rpk, st.chits};
+            unsigned long long v[12] = {pairs, n_traced, n_vis, st.boxes, st.tris, st.wrays, st.wsteps,
+                                        st.cones, st.cpk, st.rpk, st.chits, st.ctests};
 #pragma unroll
-            for (int q = 0; q < 11; ++q) {
+            for (int q = 0; q < 12; ++q) {
                 unsigned long long a = v[q];
                 for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
                 if (lane == 0) atomicAdd(&ctr->pairs + q, a);
