@@ -279,10 +279,13 @@ __device__ __forceinline__ void ref_box(int r, const float4* __restrict__ nbox, 
 }
 
 // greedy: open the inner child of largest surface area until kWide children
+#ifndef VPL_WIDE_OPEN
+#define VPL_WIDE_OPEN 0   // 16-wide collapse opens the inner child of 0: largest area, 1: most triangles, 2: area x triangles
+#endif
 template <int kW>
 __global__ void k_wide_expand(const int* __restrict__ F, int nF, const int2* __restrict__ child,
                               const float4* __restrict__ nbox, const uint8_t* __restrict__ collapsed,
-                              int* __restrict__ exp, int* __restrict__ nint) {
+                              const int* __restrict__ cnt, int* __restrict__ exp, int* __restrict__ nint) {
     int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f >= nF) return;
     int b = F[f];
@@ -296,6 +299,8 @@ __global__ void k_wide_expand(const int* __restrict__ F, int nF, const int2* __r
         for (int k = 0; k < cntc; ++k)
             if (is_inner_w<kW>(ref[k], collapsed)) {
                 float a = half_area(nbox[2 * ref[k]], nbox[2 * ref[k] + 1]);
+                if (kW == kWide && VPL_WIDE_OPEN == 1) a = (float)cnt[ref[k]];
+                if (kW == kWide && VPL_WIDE_OPEN == 2) a *= (float)cnt[ref[k]];
                 if (a > ba) { ba = a; best = k; }
             }
         if (best < 0) break;
@@ -597,9 +602,9 @@ int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* 
             while (nF > 0) {
                 ++levels;
                 if (fmt == 0) k_wide_expand<kWide><<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.child, w.nbox, w.collapsed,
-                                                                              w.wexp, w.nint);
+                                                                              w.cnt, w.wexp, w.nint);
                 else k_wide_expand<kWide4><<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.child, w.nbox, w.collapsed,
-                                                                         w.wexp, w.nint);
+                                                                         w.cnt, w.wexp, w.nint);
                 VPL_LAUNCHED("k_wide_expand");
                 cb = w.cub_bytes;
                 VPL_CUDA(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.nint, w.noff, nF, s));

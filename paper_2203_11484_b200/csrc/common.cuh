@@ -264,7 +264,10 @@ __device__ __forceinline__ void leaf_range(int node, int& first, int& count) {
 }
 
 constexpr int kStack = 128;  // > max tree depth, checked at build time (vpl_build_bvh)
-constexpr int kWarpStack = 512;  // >= 2 * kWide * wide levels, checked at build time (vpl_build_bvh)
+#ifndef VPL_WARP_STACK
+#define VPL_WARP_STACK 512
+#endif
+constexpr int kWarpStack = VPL_WARP_STACK;  // >= 2 * kWide * wide levels, checked at build time (vpl_build_bvh)
 
 // Any hit in (tmin, tmax), one ray per thread.
 template <bool kCount>

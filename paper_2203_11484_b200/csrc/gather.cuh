@@ -33,6 +33,9 @@ namespace vplgi {
 #ifndef VPL_GROUP
 #define VPL_GROUP 1
 #endif
+#ifndef VPL_QUAD
+#define VPL_QUAD 0          // 1: four nodes per traversal step (two children per lane)
+#endif
 #ifndef VPL_NO_ORDER
 #define VPL_NO_ORDER 0      // 1: push hit children in lane order (no near-to-far ordering)
 #endif
@@ -202,10 +205,69 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
         test_tri<kCount>(bv, x, S, tmin, 0, cache, st);
         return;
     }
-    // the stack holds inner nodes only; each step pops the top two (lanes 0-15 take the top one)
+    // the stack holds inner nodes only
     if (lane == 0) sstack[0] = bv.root;
     __syncwarp();
     int sp = 1;
+#if VPL_QUAD
+    // each step pops the top four: lanes 0-15 test the children of the 1st and 3rd entries,
+    // lanes 16-31 those of the 2nd and 4th (two children per lane)
+    while (sp > 0) {
+        const int i1 = sp - 1 - half, i2 = sp - 3 - half;
+        const int n1 = i1 >= 0 ? sstack[i1] : -1;
+        const int n2 = i2 >= 0 ? sstack[i2] : -1;
+        if (kCount && lane == 0) { st->wsteps += 1; st->cones += (sp >= 4 ? 4 : sp) * kWide; }
+        sp = max(sp - 4, 0);
+        const int coff = (lane & (kWide - 1)) << 5;
+        bool h1 = false, h2 = false;
+        int r1 = INT_MIN, a1 = 0, r2 = INT_MIN, a2 = 0;
+        if (n1 >= 0) {
+            const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)n1 << 9) + coff);
+            const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
+            r1 = __float_as_int(lo.w); a1 = __float_as_int(hi.w);
+            h1 = r1 != INT_MIN && beam_box(B, lo, hi);
+        }
+        if (n2 >= 0) {
+            const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)n2 << 9) + coff);
+            const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
+            r2 = __float_as_int(lo.w); a2 = __float_as_int(hi.w);
+            h2 = r2 != INT_MIN && beam_box(B, lo, hi);
+        }
+        const unsigned Bi1 = __ballot_sync(0xFFFFFFFFu, h1 && r1 >= 0);
+        const unsigned Bi2 = __ballot_sync(0xFFFFFFFFu, h2 && r2 >= 0);
+        unsigned Bl1 = __ballot_sync(0xFFFFFFFFu, h1 && r1 < 0);
+        unsigned Bl2 = __ballot_sync(0xFFFFFFFFu, h2 && r2 < 0);
+        if (Bi1 | Bi2) {
+            const int nA = __popc(Bi1 & 0xFFFFu), nB = __popc(Bi1 >> 16);
+            const int nC = __popc(Bi2 & 0xFFFFu), nD = __popc(Bi2 >> 16);
+            // bottom -> top: D, C, B, A (A = the old top is visited first)
+            const int base1 = sp + nD + nC + (half ? 0 : nB);
+            const int base2 = sp + (half ? 0 : nD);
+            if (h1 && r1 >= 0) {
+                const int nh = half ? nB : nA, rank = __popc(Bi1 & below & hmask);
+                const bool rev = (dir_neg >> a1) & 1u;
+                sstack[base1 + (rev ? rank : nh - 1 - rank)] = r1;
+            }
+            if (h2 && r2 >= 0) {
+                const int nh = half ? nD : nC, rank = __popc(Bi2 & below & hmask);
+                const bool rev = (dir_neg >> a2) & 1u;
+                sstack[base2 + (rev ? rank : nh - 1 - rank)] = r2;
+            }
+            sp += nA + nB + nC + nD;
+        }
+        __syncwarp();
+        while (Bl1 | Bl2) {   // hit triangle children
+            const bool first = Bl1 != 0;
+            const unsigned m = first ? Bl1 : Bl2;
+            const int k = __ffs(m) - 1;
+            if (first) Bl1 &= Bl1 - 1u; else Bl2 &= Bl2 - 1u;
+            const int tri = ~__shfl_sync(0xFFFFFFFFu, first ? r1 : r2, k) >> 3;
+            test_tri<kCount>(bv, x, S, tmin, tri, cache, st);
+            if (!__any_sync(0xFFFFFFFFu, S.pend != 0)) return;
+        }
+    }
+#else
+    // each step pops the top two (lanes 0-15 take the top one)
     while (sp > 0) {
         const int idx = sp - 1 - half;
         const int node = idx >= 0 ? sstack[idx] : -1;
@@ -244,6 +306,7 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
             if (!__any_sync(0xFFFFFFFFu, S.pend != 0)) return;
         }
     }
+#endif
 }
 
 // Resolve the pending segments of a group: beam over the group, else one beam

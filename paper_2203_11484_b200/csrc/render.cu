@@ -417,6 +417,11 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
     int grid = sms * VPL_GATHER_CTAS;  // persistent: VPL_GATHER_CTAS one-warp CTAs per SM
     SceneView sv = scene_view(d_scene, hh.n);
     BvhView bv = bvh_view(d_bvh, hh.n);
+#ifdef VPL_CARVEOUT
+    // shared-memory carveout preference (percent of the unified L1/shared array; tuning builds only)
+    VPL_CUDA(cudaFuncSetAttribute(k_gather<false>, cudaFuncAttributePreferredSharedMemoryCarveout, VPL_CARVEOUT));
+    VPL_CUDA(cudaFuncSetAttribute(k_gather<true>, cudaFuncAttributePreferredSharedMemoryCarveout, VPL_CARVEOUT));
+#endif
     if (d_ctr)
         k_gather<true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue);
     else
