@@ -257,6 +257,27 @@ VPL_API int32_t vpl_generate_rejection(const void* d_scene, const void* d_bvh, c
                                float* d_scores, double* d_mean, int64_t* d_accepted, int64_t* d_scanned,
                                int32_t* d_probe_pixels, void* d_work, size_t work_bytes, void* stream);
 
+/* NEXT f4  generate_metropolis: the Metropolis comparator (P:31-32 [r2],
+ * "distributes VPLs according to Metropolis-Hastings sampling"; SPEC
+ * S:261-269; O16, reading R24 — the paper gives no mutation
+ * details).  Pool = the pilot candidates along their Morton curve (O4
+ * quantisation over the pilot position box, ties by index); target
+ * f_j = max(s_pool[j], 0.05 * mean) with the probe scores s of
+ * vpl_generate_rejection (probes from `seed`).  `chains` chains (Philox
+ * stream 7, item = chain) start at (x0 * n_pilot) >> 32, propose
+ * j' = j + delta (mod n_pilot), delta uniform in [-radius, radius] \ {0},
+ * accept iff U < f_j' / f_j (fp64), and after `burn` steps emit every state:
+ * d_out[c * per_chain + t] = pilot[pool[j]] with flux *=
+ * (float)((n_pilot / (chains * per_chain)) * (mean_f / f_j)).
+ * d_accepted uint64: accepted proposals; d_scores float[n_pilot] and d_pool
+ * int32[n_pilot] nullable.  d_work: vpl_rejection_bytes(n_pilot) bytes.
+ * Errors: VPL_EINVAL (null, n_pilot < 2, chains / per_chain / radius < 1,
+ * burn < 0), VPL_ESMALL (short work). */
+VPL_API int32_t vpl_generate_metropolis(const void* d_scene, const void* d_bvh, const vpl_record* d_pilot,
+                                int64_t n_pilot, int64_t chains, int64_t per_chain, int64_t burn, int64_t radius,
+                                uint64_t seed, vpl_record* d_out, float* d_scores, int32_t* d_pool,
+                                uint64_t* d_accepted, void* d_work, size_t work_bytes, void* stream);
+
 /* -------------------------------------------------------------------- */
 /* test hooks: same traversal code as the gather / the walks */
 /* bits per listed pixel: ceil(n_vpls/32) words each of traced and visible */

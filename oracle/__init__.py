@@ -85,6 +85,7 @@ def lib():
             "oracle_direct": (None, [P, P, P, I64, C.c_int32, U64, F, P]),
             "oracle_probe_pixels": (None, [C.c_int, C.c_int, U64, P]),
             "oracle_rejection": (I64, [P, P, I64, P, I64, I64, U64, P, P, P, P]),
+            "oracle_metropolis": (I64, [P, P, I64, P, I64, I64, I64, I64, I64, U64, P, P, P, P]),
             "oracle_near_strata": (I64, [P, P, P, I64, I64, I64, P]),
             "oracle_walk_range": (None, [P, P, P, I64, I64, P, P]),
             "oracle_abi": (C.c_int, []),
@@ -328,6 +329,24 @@ class OracleScene:
                                      _p(sc), C.byref(mean), C.byref(scanned))
         return out[:acc], dict(accepted=int(acc), mean=float(mean.value), scores=sc[:len(pilot)],
                                n_scanned=int(scanned.value), probes=px)
+
+    # ---- O16 (Metropolis comparator, reading R24) ----
+    def metropolis(self, pilot, chains, per_chain, burn=64, radius=8, seed=None, gb=None):
+        """chains x per_chain VPLs from Metropolis chains over the Morton-ordered
+        pilot pool (O16).  Returns (vpls, info {scores, pool, accepted})."""
+        pilot = np.ascontiguousarray(pilot, VPL_DTYPE)
+        seed = self.scene.seed if seed is None else seed
+        if gb is None:
+            gb = self.gbuffer(self.probe_pixels(seed))
+        gb = np.ascontiguousarray(gb, GBUF_DTYPE)
+        n = int(chains) * int(per_chain)
+        out = np.zeros(max(n, 1), VPL_DTYPE)
+        sc = np.zeros(len(pilot), np.float32)
+        pool = np.zeros(len(pilot), np.int64)
+        acc = C.c_int64()
+        lib().oracle_metropolis(self.h, _p(gb), len(gb), _p(pilot), len(pilot), int(chains), int(per_chain),
+                                int(burn), int(radius), int(seed), _p(out), _p(sc), _p(pool), C.byref(acc))
+        return out[:n], dict(scores=sc, pool=pool, accepted=int(acc.value))
 
     def pair_visibility(self, x, y):
         x = np.ascontiguousarray(x, np.float32).reshape(-1, 3)

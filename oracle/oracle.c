@@ -74,7 +74,7 @@ uint32_t oracle_draw(uint64_t seed, uint32_t stream, uint32_t item, uint32_t j) 
 /* u32 -> float in [0, 1 - 2^-24], exact */
 static inline float u01(uint32_t x) { return (float)(x >> 8) * 0x1p-24f; }
 
-enum { STREAM_NEAR = 0, STREAM_WALK = 1, STREAM_DIRECT = 4, STREAM_PROBE = 5, STREAM_REJECT = 6 };
+enum { STREAM_NEAR = 0, STREAM_WALK = 1, STREAM_DIRECT = 4, STREAM_PROBE = 5, STREAM_REJECT = 6, STREAM_MH = 7 };
 
 /* ------------------------------------------------------------------------ */
 /* Scene                                                                     */
@@ -789,23 +789,9 @@ void oracle_probe_pixels(int W, int H, uint64_t seed, int32_t* pix /* [64] */) {
 /* lum(c) = ((c.r + c.g) + c.b) / 3 */
 static inline float lum3(const float* c) { return ((c[0] + c[1]) + c[2]) / 3.0f; }
 
-/* Score of candidate i: s_i = sum over probes q = 0..nq-1, in that order, in
- * fp32 of t_iq = ((cx*ci) / (r2 * max(r2, b^2)) * lum(Phi_i)) * lum(rho_q)
- * when the Eq. 1 term is traced (O13's cull and self-exclusion) and visible,
- * else 0 — the Eq. 1 summand of the VPL at the probe, as luminance.
- * mean = fp64 sum of the scores in index order / pilot.
- * Acceptance ([r3]'s rejection rule, made unbiased — reading R23):
- *   p_i = max(P_MIN, min(1, s_i / mean)) in fp64 (p_i = 1 when mean = 0),
- *   accept iff (double)U(draw 0 of Philox stream 6, item i) < p_i,
- * scanning in index order until `budget` are accepted (n_scanned = index of
- * the last one + 1, or pilot).  Kept flux = Phi * (float)((pilot / n_scanned)
- * / p_i): the scanned prefix stands for the whole pilot, 1/p_i undoes the
- * thinning.  Returns the number accepted (<= budget); out holds them. */
-#define REJ_P_MIN 0.05
-int64_t oracle_rejection(const OScene* s, const OGbuf* probes, int64_t nq, const OVpl* pilot, int64_t np_,
-                         int64_t budget, uint64_t seed, OVpl* out, float* scores, double* mean_out,
-                         int64_t* n_scanned_out) {
-    float* sc = scores ? scores : (float*)malloc(sizeof(float) * (size_t)(np_ > 0 ? np_ : 1));
+/* probe scores of the pilot candidates (shared by O15 and O16) */
+static void probe_scores(const OScene* s, const OGbuf* probes, int64_t nq, const OVpl* pilot, int64_t np_,
+                         float* sc) {
 #pragma omp parallel for schedule(dynamic, 8)
     for (int64_t i = 0; i < np_; i++) {
         float acc = 0.0f;
@@ -829,6 +815,26 @@ int64_t oracle_rejection(const OScene* s, const OGbuf* probes, int64_t nq, const
         }
         sc[i] = acc;
     }
+}
+
+/* Score of candidate i: s_i = sum over probes q = 0..nq-1, in that order, in
+ * fp32 of t_iq = ((cx*ci) / (r2 * max(r2, b^2)) * lum(Phi_i)) * lum(rho_q)
+ * when the Eq. 1 term is traced (O13's cull and self-exclusion) and visible,
+ * else 0 — the Eq. 1 summand of the VPL at the probe, as luminance.
+ * mean = fp64 sum of the scores in index order / pilot.
+ * Acceptance ([r3]'s rejection rule, made unbiased — reading R23):
+ *   p_i = max(P_MIN, min(1, s_i / mean)) in fp64 (p_i = 1 when mean = 0),
+ *   accept iff (double)U(draw 0 of Philox stream 6, item i) < p_i,
+ * scanning in index order until `budget` are accepted (n_scanned = index of
+ * the last one + 1, or pilot).  Kept flux = Phi * (float)((pilot / n_scanned)
+ * / p_i): the scanned prefix stands for the whole pilot, 1/p_i undoes the
+ * thinning.  Returns the number accepted (<= budget); out holds them. */
+#define REJ_P_MIN 0.05
+int64_t oracle_rejection(const OScene* s, const OGbuf* probes, int64_t nq, const OVpl* pilot, int64_t np_,
+                         int64_t budget, uint64_t seed, OVpl* out, float* scores, double* mean_out,
+                         int64_t* n_scanned_out) {
+    float* sc = scores ? scores : (float*)malloc(sizeof(float) * (size_t)(np_ > 0 ? np_ : 1));
+    probe_scores(s, probes, nq, pilot, np_, sc);
     double sum = 0.0;
     for (int64_t i = 0; i < np_; i++) sum += (double)sc[i];
     double mean = np_ > 0 ? sum / (double)np_ : 0.0;
@@ -857,6 +863,99 @@ int64_t oracle_rejection(const OScene* s, const OGbuf* probes, int64_t nq, const
     if (!scores) free(sc);
     if (n_scanned_out) *n_scanned_out = scanned;
     return o;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O16 — the Metropolis comparator (P:31-32 [r2]: "distributes VPLs according */
+/* to Metropolis-Hastings sampling"; reading R24).  The paper */
+/* gives no mutation details; this is a Metropolis-Hastings sampler over the  */
+/* pilot candidates laid out along their Morton curve (the O4 quantisation    */
+/* over the pilot's position box, ties by index), target                      */
+/* f_j = max(s_pool[j], 0.05 mean) (O15's probe scores), symmetric local      */
+/* mutation j' = j + delta (mod pilot), delta uniform in [-R, R] \ {0}.      */
+/* Chain c (Philox stream 7, item c, draws in sequence): start              */
+/* j = (x0 * pilot) >> 32; each step k = (x * 2R) >> 32, delta = k - R (k < R) */
+/* else k - R + 1, accept iff (double)U(next draw) < f_j' / f_j (fp64).      */
+/* After `burn` steps every state is emitted; flux *= (float)((pilot / N) *  */
+/* (mean_f / f_j)), mean_f = fp64 sum of f in pool order / pilot, N =       */
+/* chains * per_chain: the 1/p importance weight of the stationary law.      */
+/* Returns N; out[c * per_chain + t] is chain c's t-th emitted state.         */
+/* ------------------------------------------------------------------------ */
+#define MH_LARGE 0.3
+int64_t oracle_metropolis(const OScene* s, const OGbuf* probes, int64_t nq, const OVpl* pilot, int64_t np_,
+                          int64_t chains, int64_t per_chain, int64_t burn, int64_t R, uint64_t seed, OVpl* out,
+                          float* scores, int64_t* pool_out, int64_t* accepted_out) {
+    if (np_ < 2 || chains < 1 || per_chain < 0 || burn < 0 || R < 1) return 0;
+    float* sc = scores ? scores : (float*)malloc(sizeof(float) * (size_t)np_);
+    probe_scores(s, probes, nq, pilot, np_, sc);
+    double sum = 0.0;
+    for (int64_t i = 0; i < np_; i++) sum += (double)sc[i];
+    double mean = sum / (double)np_;
+    /* pool: Morton order of the pilot positions (O4 formula) */
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = 0; i < np_; i++)
+        for (int a = 0; a < 3; a++) {
+            if (pilot[i].pos[a] < lo[a]) lo[a] = pilot[i].pos[a];
+            if (pilot[i].pos[a] > hi[a]) hi[a] = pilot[i].pos[a];
+        }
+    float scale[3];
+    for (int a = 0; a < 3; a++) {
+        float ext = hi[a] - lo[a];
+        scale[a] = ext > 0.0f ? 1024.0f / ext : 0.0f;
+    }
+    MKey* keys = (MKey*)malloc(sizeof(MKey) * (size_t)np_);
+    for (int64_t i = 0; i < np_; i++) {
+        uint32_t q[3];
+        for (int a = 0; a < 3; a++) {
+            uint32_t qa = (uint32_t)((pilot[i].pos[a] - lo[a]) * scale[a]);
+            q[a] = qa < 1023u ? qa : 1023u;
+        }
+        keys[i].code = oracle_morton3(q[0], q[1], q[2]);
+        keys[i].idx = i;
+    }
+    qsort(keys, (size_t)np_, sizeof(MKey), mkey_cmp);
+    double* f = (double*)malloc(sizeof(double) * (size_t)np_);
+    double fsum = 0.0;
+    for (int64_t j = 0; j < np_; j++) {
+        double v = mean > 0.0 ? (double)sc[keys[j].idx] : 1.0;
+        double fl = 0.05 * mean;
+        f[j] = v > fl ? v : fl;
+        if (pool_out) pool_out[j] = keys[j].idx;
+        fsum += f[j];
+    }
+    double mean_f = fsum / (double)np_;
+    int64_t N = chains * per_chain;
+    int64_t acc_total = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : acc_total)
+    for (int64_t c = 0; c < chains; c++) {
+        uint32_t j = 0;
+        uint32_t x0 = oracle_draw(seed, STREAM_MH, (uint32_t)c, j++);
+        int64_t cur = (int64_t)(((uint64_t)x0 * (uint64_t)np_) >> 32);
+        for (int64_t t = 0; t < burn + per_chain; t++) {
+            double sel = (double)u01(oracle_draw(seed, STREAM_MH, (uint32_t)c, j++));
+            uint32_t xk = oracle_draw(seed, STREAM_MH, (uint32_t)c, j++);
+            int64_t nxt;
+            if (sel < MH_LARGE) {                     /* large step: uniform over the pool */
+                nxt = (int64_t)(((uint64_t)xk * (uint64_t)np_) >> 32);
+            } else {                                  /* small step: local Morton neighbour */
+                int64_t k = (int64_t)(((uint64_t)xk * (uint64_t)(2 * R)) >> 32);
+                int64_t delta = k < R ? k - R : k - R + 1;
+                nxt = ((cur + delta) % np_ + np_) % np_;
+            }
+            double u = (double)u01(oracle_draw(seed, STREAM_MH, (uint32_t)c, j++));
+            if (u < f[nxt] / f[cur]) { cur = nxt; acc_total++; }
+            if (t >= burn) {
+                OVpl* o = out + c * per_chain + (t - burn);
+                *o = pilot[keys[cur].idx];
+                float w = (float)(((double)np_ / (double)N) * (mean_f / f[cur]));
+                for (int a = 0; a < 3; a++) o->flux[a] = o->flux[a] * w;
+            }
+        }
+    }
+    if (accepted_out) *accepted_out = acc_total;
+    free(keys); free(f);
+    if (!scores) free(sc);
+    return N;
 }
 
 /* visibility of explicit (point, VPL) pairs — for sampled-pair parity */

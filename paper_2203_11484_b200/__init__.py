@@ -24,7 +24,7 @@ EXPORTS = ["vpl_abi_version", "vpl_status_string", "vpl_last_error", "vpl_launch
            "vpl_scene_upload", "vpl_scene_consts", "vpl_scene_tri_data", "vpl_bvh_bytes", "vpl_build_bvh", "vpl_classify_near_far",
            "vpl_generate_bytes", "vpl_generate_vpls", "vpl_render_gbuffer", "vpl_gather_bytes",
            "vpl_gather_indirect", "vpl_render_direct", "vpl_image_error", "vpl_rejection_bytes",
-           "vpl_generate_rejection", "vpl_visibility_dump", "vpl_closest_hit_batch", "vpl_occluded_batch",
+           "vpl_generate_rejection", "vpl_generate_metropolis", "vpl_visibility_dump", "vpl_closest_hit_batch", "vpl_occluded_batch",
            "vpl_philox_batch"]
 
 
@@ -102,6 +102,7 @@ def load_library(path: str | os.PathLike | None = None):
         "vpl_render_direct": (I32, [P, P, P, P, I32, I32, I32, I32, C.c_uint64, I32, P, P]),
         "vpl_image_error": (I32, [P, P, I64, P, P, SZ, P]),
         "vpl_rejection_bytes": (I32, [I64, P]),
+        "vpl_generate_metropolis": (I32, [P, P, P, I64, I64, I64, I64, I64, C.c_uint64, P, P, P, P, P, SZ, P]),
         "vpl_generate_rejection": (I32, [P, P, P, I64, I64, C.c_uint64, P, P, P, P, P, P, P, SZ, P]),
         "vpl_visibility_dump": (I32, [P, P, P, P, I32, P, I32, P, P, P]),
         "vpl_closest_hit_batch": (I32, [P, P, P, P, I64, F, F, P, P, P]),
@@ -323,6 +324,30 @@ def generate_rejection(scene, bvh, pilot, budget, seed, stream=None):
     a = int(acc.item())
     return out[: a * VPL_RECORD_BYTES].view(-1, VPL_RECORD_BYTES), dict(
         accepted=a, mean=float(mean.item()), scores=scores[:n], n_scanned=int(scanned.item()), probes=probes)
+
+
+def generate_metropolis(scene, bvh, pilot, chains, per_chain, burn=64, radius=8, seed=0, stream=None):
+    """NEXT f4: chains x per_chain VPLs from Metropolis chains over the pilot
+    (vpl_generate_metropolis).  Returns (vpls uint8 [N, 48], info {accepted,
+    scores, pool}).  Synchronises."""
+    dev = scene.device
+    pilot = pilot.contiguous().view(-1, VPL_RECORD_BYTES)
+    n = pilot.shape[0]
+    N = int(chains) * int(per_chain)
+    wb = C.c_size_t()
+    _check(load_library().vpl_rejection_bytes(n, C.byref(wb)), "vpl_rejection_bytes")
+    work = torch.empty(max(wb.value, 1), dtype=torch.uint8, device=dev)
+    out = torch.empty(max(N, 1) * VPL_RECORD_BYTES, dtype=torch.uint8, device=dev)
+    scores = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    pool = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    acc = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(load_library().vpl_generate_metropolis(_ptr(scene), _ptr(bvh), _ptr(pilot), n, int(chains), int(per_chain),
+                                                  int(burn), int(radius), int(seed), _ptr(out), _ptr(scores),
+                                                  _ptr(pool), _ptr(acc), _ptr(work), work.numel(), _stream(stream)),
+           "vpl_generate_metropolis")
+    torch.cuda.synchronize(dev)
+    return out[: N * VPL_RECORD_BYTES].view(-1, VPL_RECORD_BYTES), dict(accepted=int(acc.item()), scores=scores[:n],
+                                                                         pool=pool[:n])
 
 
 IMAGE_ERROR_WORK_BYTES = 8 * 4 * 592

@@ -11,7 +11,8 @@ from __future__ import annotations
 
 import torch
 
-from . import (Renderer, all_tiles, gather_indirect, generate_rejection, generate_vpls, image_error)
+from . import (Renderer, all_tiles, gather_indirect, generate_metropolis, generate_rejection, generate_vpls,
+               image_error)
 
 
 def _timed(fn):
@@ -24,10 +25,12 @@ def _timed(fn):
 
 
 def compare_estimators(scene, M_list=(1024, 4096), ref_M=262144, ref_seed=None, device="cuda", return_images=False,
-                       pilot_factor=4):
+                       pilot_factor=4, mh_burn=64, mh_radius=16):
     """Returns {"ref": {...}, "ref_hybrid": {...}, "runs": [{"M", "hybrid",
     "hybrid_vs_own", "ir", "rejection"}]}.  Rejection (f3, O15): an IR pilot of
-    pilot_factor * M candidates scored at 64 probe pixels, M kept.  Hybrid: near fraction K_near/M of the scene's
+    pilot_factor * M candidates scored at 64 probe pixels, M kept.  Metropolis
+    (f4, O16): min(256, M) chains over the same pilot pool, burn-in mh_burn,
+    mutation radius mh_radius, M states emitted.  Hybrid: near fraction K_near/M of the scene's
     own configuration; IR: all patches FAR (K = 0, M_far = M, budget rule O10).
     References (independent seed ref_seed, default scene.seed + 1000): dense
     IR with ref_M VPLs (the paper's reference) and the dense hybrid with
@@ -70,8 +73,13 @@ def compare_estimators(scene, M_list=(1024, 4096), ref_M=262144, ref_seed=None, 
                                                            s.max_depth, s.rr, s.seed, max_out=pilot_factor * M))
         (rv, r_info), rg = _timed(lambda: generate_rejection(r.scene, r.bvh, pv, M, s.seed))
         (j_img, _), jt = _timed(lambda: gather_indirect(r.scene, r.bvh, r.gbuf, rv, tiles, W, H, 16, 16))
+        # Metropolis comparator (f4): chains over the same pilot, M states emitted
+        chains = min(256, M)
+        (mv, m_info), mg = _timed(lambda: generate_metropolis(r.scene, r.bvh, pv, chains, M // chains, mh_burn,
+                                                              mh_radius, s.seed))
+        (k_img, _), kt = _timed(lambda: gather_indirect(r.scene, r.bvh, r.gbuf, mv, tiles, W, H, 16, 16))
         if return_images:
-            images[M] = (h_img.clone(), i_img.clone(), j_img.clone())
+            images[M] = (h_img.clone(), i_img.clone(), j_img.clone(), k_img.clone())
         out["runs"].append({
             "M": M,
             "hybrid": dict(image_error(h_img, ref_img), K=h_info["K"], M_far=h_info["M_far"], gen_ms=hg,
@@ -80,6 +88,9 @@ def compare_estimators(scene, M_list=(1024, 4096), ref_M=262144, ref_seed=None, 
             "ir": dict(image_error(i_img, ref_img), K=i_info["K"], M_far=i_info["M_far"], gen_ms=ig, gather_ms=it),
             "rejection": dict(image_error(j_img, ref_img), pilot=pilot_factor * M, accepted=r_info["accepted"],
                               n_scanned=r_info["n_scanned"], gen_ms=pg + rg, gather_ms=jt),
+            "metropolis": dict(image_error(k_img, ref_img), pilot=pilot_factor * M, chains=chains,
+                               per_chain=M // chains, accept_rate=m_info["accepted"] / (chains * (mh_burn + M // chains)),
+                               gen_ms=pg + mg, gather_ms=kt),
         })
     if return_images:
         images["ref"] = ref_img

@@ -703,3 +703,59 @@ def test_rejection_is_unbiased_in_power():
     assert abs(m - tot) < 4 * se + 1e-6 * tot, (m, tot, se)
     assert abs(np.mean(counts) - p.sum()) < 4 * np.std(counts) / math.sqrt(len(counts)) + 1e-9
     assert info["n_scanned"] == len(pilot)
+
+
+# ---------------------------------------------------------------- O16 Metropolis comparator (reading R24)
+def _c1_pilot(M=1024):
+    s1 = scenegen.make_scene(1)
+    o1 = oracle.OracleScene(s1)
+    pilot, _ = o1.generate_vpls(np.zeros(s1.n_tris, np.uint8), M=M, K_near=0)
+    return o1, pilot
+
+
+def test_metropolis_flat_target_accepts_everything():
+    """a uniform target gives acceptance rate 1.0 (every ratio is 1)."""
+    s, o = _gather_setup()
+    g = _gb(np.array([[0.0, 0, 0], [1.0, 0, 0.5]], np.float32))
+    pv = np.concatenate([_vpl([0.2, 2.0, 0.1])] * 50)
+    out, info = o.metropolis(pv, chains=4, per_chain=10, burn=5, radius=3, seed=1, gb=g)
+    assert info["accepted"] == 4 * (5 + 10) and len(out) == 40
+    assert np.array_equal(out["flux"], np.repeat(pv["flux"][:1], 40, 0) * np.float32(50 / 40))
+
+
+def test_metropolis_pool_is_morton_ordered_and_stationary_law_is_f():
+    """The pool follows the O4 Morton order of the pilot positions; with a
+    wide mutation the chains' visit frequencies over f-quantile bins match
+    f (the stationary law) to 5%."""
+    o1, pilot = _c1_pilot()
+    out, info = o1.metropolis(pilot, chains=64, per_chain=3000, burn=300, radius=300, seed=5)
+    pos = pilot["pos"][info["pool"]].astype(np.float32)
+    lo, hi = pos.min(0), pos.max(0)
+    scale = np.where(hi - lo > 0, np.float32(1024.0) / (hi - lo), 0).astype(np.float32)
+    q = np.minimum(((pos - lo).astype(np.float32) * scale).astype(np.uint32), 1023)
+    codes = [oracle.morton3(int(a), int(b), int(c)) for a, b, c in q]
+    assert all(x <= y for x, y in zip(codes, codes[1:]))
+    sc = info["scores"].astype(np.float64)
+    f = np.maximum(sc, 0.05 * sc.mean())
+    # visited pool index of every emitted record: match by walk/position
+    key = {tuple(pilot["pos"][i].tolist()) + (int(pilot["walk"][i]),): i for i in range(len(pilot))}
+    vis = np.array([key[tuple(r["pos"].tolist()) + (int(r["walk"]),)] for r in out])
+    bins = np.digitize(f, np.quantile(f, [0.25, 0.5, 0.75]))
+    for b in range(4):
+        expect = f[bins == b].sum() / f.sum()
+        got = np.isin(vis, np.flatnonzero(bins == b)).mean()
+        assert abs(got - expect) < 0.05 * expect + 0.01, (b, got, expect)
+
+
+def test_metropolis_is_unbiased_in_power():
+    """E[sum of emitted flux] = sum of pilot flux under the stationary law
+    (importance weight (pilot / N) * mean_f / f): mean over 60 seeds within 4 sigma."""
+    o1, pilot = _c1_pilot(512)
+    gb = o1.gbuffer(o1.probe_pixels(seed=1))
+    tot = pilot["flux"][:, 0].astype(np.float64).sum()
+    sums = []
+    for seed in range(60):
+        out, _ = o1.metropolis(pilot, chains=32, per_chain=64, burn=64, radius=128, seed=seed, gb=gb)
+        sums.append(out["flux"][:, 0].astype(np.float64).sum())
+    m, se = np.mean(sums), np.std(sums) / math.sqrt(len(sums))
+    assert abs(m - tot) < 4 * se + 1e-3 * tot, (m, tot, se)
