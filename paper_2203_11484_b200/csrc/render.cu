@@ -23,16 +23,68 @@ __global__ void k_gbuffer(SceneView sv, BvhView bv, TileMap tm, vpl_gpoint* __re
 // groups of nearby VPLs, so the shadow segments of a warp form a narrow beam
 // (gather.cuh).  fp32 two-level accumulation: a per-batch partial is folded
 // into the running total every 256 VPLs (groups never straddle a batch).
+// VPL clusters: 32 consecutive VPLs of the Morton-ordered copy, bounded by
+// their position box and normal box (4 float4: ylo, yhi, nlo, nhi).  A lane
+// can trace some VPL of the cluster only if cx = n_x.(y - x) > 0 and
+// ci = n_i.(x - y) > 0 are both possible over the boxes; the bounds are
+// evaluated with a relative margin far above the fp32 rounding of O13's cull,
+// so a skipped cluster holds no traced pair (the image is unchanged bitwise).
+constexpr int kCluster = 32;
+__device__ __forceinline__ bool cluster_may_trace(const float4* __restrict__ cb, f3 x, f3 nx) {
+    const float4 ylo = __ldg(cb), yhi = __ldg(cb + 1), nlo = __ldg(cb + 2), nhi = __ldg(cb + 3);
+    // max over y in the box of n_x.(y - x): per axis the larger of n*(lo - x), n*(hi - x)
+    const float ax = fmaxf(nx.x * (ylo.x - x.x), nx.x * (yhi.x - x.x));
+    const float ay = fmaxf(nx.y * (ylo.y - x.y), nx.y * (yhi.y - x.y));
+    const float az = fmaxf(nx.z * (ylo.z - x.z), nx.z * (yhi.z - x.z));
+    // max over n in the normal box, y in the position box of n.(x - y): corner products per axis
+    const float dxl = x.x - yhi.x, dxh = x.x - ylo.x, dyl = x.y - yhi.y, dyh = x.y - ylo.y;
+    const float dzl = x.z - yhi.z, dzh = x.z - ylo.z;
+    const float bx = fmaxf(fmaxf(nlo.x * dxl, nlo.x * dxh), fmaxf(nhi.x * dxl, nhi.x * dxh));
+    const float by = fmaxf(fmaxf(nlo.y * dyl, nlo.y * dyh), fmaxf(nhi.y * dyl, nhi.y * dyh));
+    const float bz = fmaxf(fmaxf(nlo.z * dzl, nlo.z * dzh), fmaxf(nhi.z * dzl, nhi.z * dzh));
+    const float scale = fmax3(fabsf(x.x), fabsf(x.y), fabsf(x.z)) +
+                        fmax3(fmaxf(fabsf(ylo.x), fabsf(yhi.x)), fmaxf(fabsf(ylo.y), fabsf(yhi.y)),
+                              fmaxf(fabsf(ylo.z), fabsf(yhi.z)));
+    const float m = 1e-4f * scale;   // >> the rounding of d = y - x and of the two dots
+    return (ax + ay) + az > -m && (bx + by) + bz > -m;
+}
+__global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, float4* __restrict__ cb) {
+    const int c = blockIdx.x, lane = threadIdx.x;
+    const int i = c * kCluster + lane;
+    const float inf = __int_as_float(0x7f800000);
+    float4 a = make_float4(inf, inf, inf, 0.0f), b = make_float4(-inf, -inf, -inf, 0.0f);
+    float4 na = a, nb = b;
+    if (i < M) {
+        const float4* p = (const float4*)(v + i);
+        const float4 y = p[0], n = p[1];
+        a = make_float4(y.x, y.y, y.z, 0.0f); b = a;
+        na = make_float4(n.x, n.y, n.z, 0.0f); nb = na;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        a.x = fminf(a.x, __shfl_xor_sync(0xFFFFFFFFu, a.x, o)); b.x = fmaxf(b.x, __shfl_xor_sync(0xFFFFFFFFu, b.x, o));
+        a.y = fminf(a.y, __shfl_xor_sync(0xFFFFFFFFu, a.y, o)); b.y = fmaxf(b.y, __shfl_xor_sync(0xFFFFFFFFu, b.y, o));
+        a.z = fminf(a.z, __shfl_xor_sync(0xFFFFFFFFu, a.z, o)); b.z = fmaxf(b.z, __shfl_xor_sync(0xFFFFFFFFu, b.z, o));
+        na.x = fminf(na.x, __shfl_xor_sync(0xFFFFFFFFu, na.x, o)); nb.x = fmaxf(nb.x, __shfl_xor_sync(0xFFFFFFFFu, nb.x, o));
+        na.y = fminf(na.y, __shfl_xor_sync(0xFFFFFFFFu, na.y, o)); nb.y = fmaxf(nb.y, __shfl_xor_sync(0xFFFFFFFFu, nb.y, o));
+        na.z = fminf(na.z, __shfl_xor_sync(0xFFFFFFFFu, na.z, o)); nb.z = fmaxf(nb.z, __shfl_xor_sync(0xFFFFFFFFu, nb.z, o));
+    }
+    if (lane == 0) { cb[4 * c] = a; cb[4 * c + 1] = b; cb[4 * c + 2] = na; cb[4 * c + 3] = nb; }
+}
+
 // One warp per CTA: the traversal stack is then at a fixed shared-memory
 // address (no per-warp base to keep live in a register), and 32 one-warp
 // CTAs fill an SM at the 64-register budget.
+#ifndef VPL_CLUSTER_CULL
+#define VPL_CLUSTER_CULL 1   // skip 32-VPL clusters no lane of the warp can trace
+#endif
 #ifndef VPL_GATHER_CTAS
 #define VPL_GATHER_CTAS 32
 #endif
 template <bool kCount>
 __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb,
                                                 const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
-                                                vpl_counters* __restrict__ ctr, int* __restrict__ queue) {
+                                                vpl_counters* __restrict__ ctr, int* __restrict__ queue,
+                                                const float4* __restrict__ clusters) {
     __shared__ int sstack[kWarpStack];
     __shared__ float s_acc[3][32];   // running per-lane totals (kept out of the register budget)
     const int lane = threadIdx.x;
@@ -67,6 +119,11 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 float part[3] = {0.0f, 0.0f, 0.0f};
                 const int i1 = min(M, i0 + 256);
                 for (int i = i0; i < i1;) {
+                    if (clusters && (i & (kCluster - 1)) == 0 &&
+                        !__any_sync(0xFFFFFFFFu, active && cluster_may_trace(clusters + 4 * (i / kCluster), x, nx))) {
+                        i = min(i + kCluster, i1);     // no lane can trace any VPL of this cluster
+                        continue;
+                    }
                     f3 yk[kGroup];
                     const int gsz = group_at(vpls, i, i1, xr, yk);
                     unsigned vis;
@@ -308,6 +365,7 @@ __global__ void k_image_err_final(const double* __restrict__ part, int nb, doubl
 struct GatherWork {
     int* queue;
     unsigned* box;
+    float4* clusters;
     uint32_t *keys, *keys2;
     int32_t *idx, *idx2;
     vpl_record* sorted;
@@ -324,6 +382,7 @@ static size_t gather_layout(int32_t M, char* base, GatherWork* w) {
     w->idx = b.take<int32_t>(m);
     w->idx2 = b.take<int32_t>(m);
     w->sorted = b.take<vpl_record>(m);
+    w->clusters = b.take<float4>(4 * ((m + 31) / 32));
     size_t c = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
                                     (int32_t*)nullptr, (int)m, 0, 30);
@@ -411,6 +470,14 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
         VPL_LAUNCHED("k_vpl_permute");
         vp = w.sorted;
     }
+    const float4* clusters = nullptr;
+#if VPL_CLUSTER_CULL
+    if (n_vpls > 0) {
+        k_vpl_clusters<<<(n_vpls + kCluster - 1) / kCluster, kCluster, 0, s>>>(vp, n_vpls, w.clusters);
+        VPL_LAUNCHED("k_vpl_clusters");
+        clusters = w.clusters;
+    }
+#endif
     int dev = 0, sms = 148;
     VPL_CUDA(cudaGetDevice(&dev));
     VPL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -423,9 +490,9 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
     VPL_CUDA(cudaFuncSetAttribute(k_gather<true>, cudaFuncAttributePreferredSharedMemoryCarveout, VPL_CARVEOUT));
 #endif
     if (d_ctr)
-        k_gather<true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue);
+        k_gather<true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue, clusters);
     else
-        k_gather<false><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue);
+        k_gather<false><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue, clusters);
     VPL_LAUNCHED("k_gather");
     return VPL_OK;
 }
