@@ -83,6 +83,30 @@ __device__ __forceinline__ bool beam_box(const Beam& B, float4 lo, float4 hi) {
     return sn <= sf;
 }
 
+#ifndef VPL_MT_EARLY
+#define VPL_MT_EARLY 0      // 1: skip the second half of MT when no active lane's u lies in [0, 1]
+#endif
+#ifndef VPL_BEAM_SMEM
+#define VPL_BEAM_SMEM 0     // 1: keep the beam coefficients in shared memory (frees ~15 registers)
+#endif
+// warp-uniform beam in shared memory: F0 = (a0, s_lo), F1 = (b0, s_hi), F2 = (a1, pos bits), F3 = (b1, 0)
+__device__ __forceinline__ float4 lds4(unsigned a) {
+    float4 r;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ bool beam_box_s(unsigned sb, float4 lo, float4 hi) {
+    const float4 F0 = lds4(sb), F1 = lds4(sb + 16), F2 = lds4(sb + 32), F3 = lds4(sb + 48);
+    const unsigned pos = __float_as_uint(F2.w);
+    const bool px = pos & 1u, py = pos & 2u, pz = pos & 4u;
+    float s0x = fmaf(px ? lo.x : hi.x, F0.x, -F1.x), s1x = fmaf(px ? hi.x : lo.x, F2.x, -F3.x);
+    float s0y = fmaf(py ? lo.y : hi.y, F0.y, -F1.y), s1y = fmaf(py ? hi.y : lo.y, F2.y, -F3.y);
+    float s0z = fmaf(pz ? lo.z : hi.z, F0.z, -F1.z), s1z = fmaf(pz ? hi.z : lo.z, F2.z, -F3.z);
+    float sn = fmax3(s0x, s0y, fmaxf(s0z, F0.w));
+    float sf = fmin3(s1x, s1y, fminf(s1z, F1.w));
+    return sn <= sf;
+}
+
 // One lane's shadow segments of a group: origin x (the receiver), direction
 // d_k = (y_k - x)/|y_k - x|, t in (eps, |y_k - x| - eps)  (O9).
 struct Segs {
@@ -100,9 +124,28 @@ __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, 
                                             float4 c, TravStats* st) {
     const f3 v0 = xyz(a), e1 = xyz(b), e2 = xyz(c);
     const f3 s = o - v0;
+    unsigned hit = 0;
+#if VPL_MT_EARLY && VPL_GROUP == 1
+    // single segment: u first; the rest of O9 only if some active lane's u is in [0, 1]
+    if (mask & 1u) {
+        if (kCount) st->tris += 1;
+        const f3 d = S.d[0];
+        const f3 pv = cross(d, e2);
+        const float det = dot(e1, pv);
+        const float inv = 1.0f / det;
+        const float u = dot(s, pv) * inv;
+        // (det == 0 needs no test of its own: u is then NaN or +-inf and fails u >= 0 or u <= 1)
+        const bool uok = (u >= 0.0f) & (u <= 1.0f);
+        if (__any_sync(__activemask(), uok)) {
+            const f3 q = cross(s, e1);
+            const float v = dot(d, q) * inv;
+            const float t = dot(e2, q) * inv;
+            if (uok & (v >= 0.0f) & ((u + v) <= 1.0f) & (t > tmin) & (t < S.tmax[0])) hit = 1u;
+        }
+    }
+#else
     const f3 q = cross(s, e1);
     const float tq = dot(e2, q);
-    unsigned hit = 0;
 #pragma unroll
     for (int k = 0; k < kGroup; ++k) {
         if (mask & (1u << k)) {
@@ -119,6 +162,7 @@ __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, 
                 hit |= 1u << k;
         }
     }
+#endif
     return hit;
 }
 
@@ -205,6 +249,16 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
         test_tri<kCount>(bv, x, S, tmin, 0, cache, st);
         return;
     }
+#if VPL_BEAM_SMEM
+    const unsigned sbeam = (unsigned)__cvta_generic_to_shared(sstack + kWarpStack);
+    if (lane == 0) {
+        float4* F = (float4*)(sstack + kWarpStack);
+        F[0] = make_float4(B.a0[0], B.a0[1], B.a0[2], B.s_lo);
+        F[1] = make_float4(B.b0[0], B.b0[1], B.b0[2], B.s_hi);
+        F[2] = make_float4(B.a1[0], B.a1[1], B.a1[2], __uint_as_float(B.pos));
+        F[3] = make_float4(B.b1[0], B.b1[1], B.b1[2], 0.0f);
+    }
+#endif
     // the stack holds inner nodes only
     if (lane == 0) sstack[0] = bv.root;
     __syncwarp();
@@ -280,7 +334,11 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
             const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
             ref = __float_as_int(lo.w);
             axis = __float_as_int(hi.w);
+#if VPL_BEAM_SMEM
+            hit = ref != INT_MIN && beam_box_s(sbeam, lo, hi);
+#else
             hit = ref != INT_MIN && beam_box(B, lo, hi);
+#endif
         }
         const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
         unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);

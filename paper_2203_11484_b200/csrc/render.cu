@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                                                 const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
                                                 vpl_counters* __restrict__ ctr, int* __restrict__ queue,
                                                 const float4* __restrict__ clusters) {
-    __shared__ int sstack[kWarpStack];
+    __shared__ __align__(16) int sstack[kWarpStack + 16];   // traversal stack + the warp's beam (VPL_BEAM_SMEM)
     __shared__ float s_acc[3][32];   // running per-lane totals (kept out of the register budget)
     const int lane = threadIdx.x;
     const int64_t nw = tm.n_warps();
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
 __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict__ gb, const vpl_record* __restrict__ vpls,
                           int32_t M, const int32_t* __restrict__ pixels, int32_t n_px, uint32_t* __restrict__ tbits,
                           uint32_t* __restrict__ vbits) {
-    __shared__ int s_stack[2][kWarpStack];
+    __shared__ __align__(16) int s_stack[2][kWarpStack + 16];
     int* sstack = s_stack[threadIdx.x >> 5];
     int64_t words = (M + 31) / 32;
     OccluderCache cache;
