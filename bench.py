@@ -105,6 +105,21 @@ OPS = {"pairs": 21,        # d = y - x (3), r^2 (5), cx (5), ci (5), tri / cx / 
        "tri_tests": 52}    # exact Moller-Trumbore (O9): 44 FMUL/FADD + 1 div + 7 compares
 
 
+def measured_traffic():
+    """dram read + write bytes of one C4 gather launch from the committed ncu
+    capture (profiles/r01_gather_c4_dram.csv), or None."""
+    import csv
+    f = ROOT / "profiles" / "r01_gather_c4_dram.csv"
+    if not f.exists():
+        return None
+    tot, seen = 0.0, 0
+    for r in csv.reader(f.read_text().splitlines()):
+        if len(r) > 14 and r[12] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(r[14].replace(",", ""))
+            seen += 1
+    return tot if seen == 2 else None
+
+
 def algorithmic_ops(c: dict) -> int:
     return sum(c[k] * v for k, v in OPS.items())
 
@@ -276,7 +291,8 @@ def run_ours(args):
                              cache_tests_per_traced=c["cache_tests"] / max(traced, 1)),
             "roofline": {"bound": "alu", "kernel": "k_gather", "achieved": achieved / 1e12,
                          "peak": peak_ops / 1e12, "unit": "Tops/s", "frac": achieved / peak_ops,
-                         "traffic": None,
+                         "traffic": measured_traffic() if args.config == 4 else None,
+                         "traffic_unit": "bytes per launch (dram read + write, profiles/r01_gather_c4_dram.csv)",
                          "peak_source": f"derived: {sm_count} SMs x 128 lanes/clk x {f_max / 1e6:.0f} MHz "
                                         f"(issue roof, DESIGN.md §5)"},
             "e2e": {"value": pairs_per_step / (t_e2e * 1e-3), "unit": UNIT, "ms": t_e2e,
