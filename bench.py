@@ -95,14 +95,35 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------- algorithmic op counts
 # Per-unit thread-op counts: the arithmetic the method itself prescribes per
-# unit of work.  The exact fp32 contract (O0) forbids FMA
-# contraction in the Eq. 1 terms and in Moller-Trumbore, so those count as
-# separate FMUL/FADD; divisions and square roots count as one op each.
-OPS = {"pairs": 21,        # d = y - x (3), r^2 (5), cx (5), ci (5), tri / cx / ci tests (3)   (O13)
-       "traced": 13,       # sqrt, 3 div (direction), tmax, tmax > eps, w (4), 3 FFMA accumulate (O9, O13)
-       "box_tests": 17,    # per-ray slab test, centre/half-extent form: 3 FFMA + 3 FMUL + 6 FADD + 4 min/max + 1 cmp
-       "cone_tests": 17,   # beam x child box: 6 FFMA + 6 SEL + 4 min/max + 1 cmp (gather.cuh beam_box)
-       "tri_tests": 52}    # exact Moller-Trumbore (O9): 44 FMUL/FADD + 1 div + 7 compares
+# unit of work, split by the SM pipe that executes it.  The
+# exact fp32 contract (O0) forbids FMA contraction in the Eq. 1 terms and in
+# Moller-Trumbore, so those count as separate FMUL/FADD; square roots and
+# divisions count as one MUFU op each.  (fma, alu, mufu) per unit:
+OPS = {"pairs": (18, 3, 0),       # d (3), r^2 (5), cx (5), ci (5) | tri, cx, ci tests                 (O13)
+       "traced": (6, 2, 4),       # tmax, cx*ci, r2*max, 3 FFMA | test, max | sqrt, 3 div (direction)    (O9, O13)
+       "box_tests": (12, 5, 0),   # per-ray slab (centre/half-extent): 3 FFMA + 3 FMUL + 6 FADD | 4 min/max + cmp
+       "cone_tests": (6, 11, 0),  # beam x child box: 6 FFMA | 6 SEL + 4 min/max + 1 cmp (gather.cuh beam_box)
+       "tri_tests": (44, 7, 1)}   # exact Moller-Trumbore (O9): 44 FMUL/FADD | 7 compares | 1 division
+
+# Pipe rates in thread-ops per clock per SM, measured on this pool's B200
+# (tools/pipebench.cu, profiles/r01_pipebench.jsonl): FFMA/FMUL/FADD 126,
+# FMNMX/FSETP/FSEL/LOP3 64, MUFU.RCP 14.6; instruction issue 4 warps x 32.
+PIPE = {"fma": 128.0, "alu": 64.0, "mufu": 16.0, "issue": 128.0}
+
+
+def algorithmic_ops(c: dict) -> int:
+    return sum(c[k] * sum(v) for k, v in OPS.items())
+
+
+def roof_seconds(c: dict, sms: int, f_hz: float) -> tuple[float, str]:
+    """T_roof = max over pipes of ops / (rate * SMs * f); returns (T, binding pipe)."""
+    fma = sum(c[k] * v[0] for k, v in OPS.items())
+    alu = sum(c[k] * v[1] for k, v in OPS.items())
+    mufu = sum(c[k] * v[2] for k, v in OPS.items())
+    t = {"fma": fma / PIPE["fma"], "alu": alu / PIPE["alu"], "mufu": mufu / PIPE["mufu"],
+         "issue": (fma + alu + mufu) / PIPE["issue"]}
+    k = max(t, key=t.get)
+    return t[k] / (sms * f_hz), k
 
 
 def measured_traffic():
@@ -118,10 +139,6 @@ def measured_traffic():
             tot += float(r[14].replace(",", ""))
             seen += 1
     return tot if seen == 2 else None
-
-
-def algorithmic_ops(c: dict) -> int:
-    return sum(c[k] * v for k, v in OPS.items())
 
 
 # ---------------------------------------------------------------------------- our arm
@@ -267,9 +284,11 @@ def run_ours(args):
         sm_count = V.device_info()["sm_count"]
         clocks = clk.summary()
         f_max = (clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
-        peak_ops = sm_count * 128 * f_max                      # 4 SMSP x 32 lanes issue per clock
         ops = algorithmic_ops(ctr) / max(world, 1)              # per launch (one rank's share)
+        share = {k: v / max(world, 1) for k, v in ctr.items()}
+        t_roof, binding = roof_seconds(share, sm_count, f_max)
         achieved = ops / (t_gather * 1e-3)
+        peak_ops = ops / t_roof                                  # the pipe roof for this op mix
         c = ctr
         pairs, traced = c["pairs"], c["traced"]
         out = {
@@ -291,10 +310,13 @@ def run_ours(args):
                              cache_tests_per_traced=c["cache_tests"] / max(traced, 1)),
             "roofline": {"bound": "alu", "kernel": "k_gather", "achieved": achieved / 1e12,
                          "peak": peak_ops / 1e12, "unit": "Tops/s", "frac": achieved / peak_ops,
+                         "binding_pipe": binding, "t_roof_ms": t_roof * 1e3,
                          "traffic": measured_traffic() if args.config == 4 else None,
                          "traffic_unit": "bytes per launch (dram read + write, profiles/r01_gather_c4_dram.csv)",
-                         "peak_source": f"derived: {sm_count} SMs x 128 lanes/clk x {f_max / 1e6:.0f} MHz "
-                                        f"(issue roof, DESIGN.md §5)"},
+                         "peak_source": f"derived: {sm_count} SMs x {f_max / 1e6:.0f} MHz x measured pipe rates "
+                                        f"(FMA 128, ALU 64, MUFU 16, issue 128 thread-ops/clk/SM; "
+                                        f"profiles/r01_pipebench.jsonl), max over pipes for this op mix "
+                                        f"(DESIGN.md §5)"},
             "e2e": {"value": pairs_per_step / (t_e2e * 1e-3), "unit": UNIT, "ms": t_e2e,
                     "h2d_bytes_per_step": int(s.verts.nbytes + s.albedo.nbytes),
                     "d2h_bytes_per_step": int(W * H * 3 * 4)},
