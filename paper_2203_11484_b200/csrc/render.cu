@@ -74,6 +74,9 @@ __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, floa
 // One warp per CTA: the traversal stack is then at a fixed shared-memory
 // address (no per-warp base to keep live in a register), and 32 one-warp
 // CTAs fill an SM at the 64-register budget.
+#ifndef VPL_NX_SMEM
+#define VPL_NX_SMEM 0   // 1: keep the receiver normal / triangle in shared memory (fewer live registers)
+#endif
 #ifndef VPL_CLUSTER_CULL
 #define VPL_CLUSTER_CULL 1   // skip 32-VPL clusters no lane of the warp can trace
 #endif
@@ -87,6 +90,10 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                                                 const float4* __restrict__ clusters) {
     __shared__ __align__(16) int sstack[kWarpStack + 16];   // traversal stack + the warp's beam (VPL_BEAM_SMEM)
     __shared__ float s_acc[3][32];   // running per-lane totals (kept out of the register budget)
+#if VPL_NX_SMEM
+    __shared__ __align__(16) float4 s_nx[32];
+    const unsigned s_nx_addr = (unsigned)__cvta_generic_to_shared(&s_nx[threadIdx.x]);
+#endif
     const int lane = threadIdx.x;
     const int64_t nw = tm.n_warps();
     const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
@@ -106,6 +113,10 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             active = tri_x >= 0 && __float_as_int(b.w) != 0;
             x = xyz(a); nx = xyz(b);
         }
+#if VPL_NX_SMEM
+        s_nx[lane] = make_float4(nx.x, nx.y, nx.z, __int_as_float(tri_x));
+        __syncwarp();
+#endif
         s_acc[0][lane] = 0.0f; s_acc[1][lane] = 0.0f; s_acc[2][lane] = 0.0f;
         OccluderCache cache;
         TravStats st;
@@ -119,8 +130,14 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 float part[3] = {0.0f, 0.0f, 0.0f};
                 const int i1 = min(M, i0 + 256);
                 for (int i = i0; i < i1;) {
+#if VPL_NX_SMEM
+                    if (clusters && (i & (kCluster - 1)) == 0 &&
+                        !__any_sync(0xFFFFFFFFu, active && cluster_may_trace(clusters + 4 * (i / kCluster), x,
+                                                                             xyz(lds4(s_nx_addr))))) {
+#else
                     if (clusters && (i & (kCluster - 1)) == 0 &&
                         !__any_sync(0xFFFFFFFFu, active && cluster_may_trace(clusters + 4 * (i / kCluster), x, nx))) {
+#endif
                         i = min(i + kCluster, i1);     // no lane can trace any VPL of this cluster
                         continue;
                     }
@@ -128,7 +145,15 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                     const int gsz = group_at(vpls, i, i1, xr, yk);
                     unsigned vis;
                     float w[kGroup];
-                    const unsigned tr = shade_group<kCount>(bv, vpls, i, gsz, yk, x, nx, tri_x, active, eps, b2, cache,
+#if VPL_NX_SMEM
+                    const float4 nt = lds4(s_nx_addr);   // receiver normal + triangle, re-read per VPL (registers)
+                    const f3 nxv = xyz(nt);
+                    const int trv = __float_as_int(nt.w);
+#else
+                    const f3 nxv = nx;
+                    const int trv = tri_x;
+#endif
+                    const unsigned tr = shade_group<kCount>(bv, vpls, i, gsz, yk, x, nxv, trv, active, eps, b2, cache,
                                                             sstack, &st, &vis, w);
                     if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
 #pragma unroll
