@@ -83,6 +83,15 @@ __device__ __forceinline__ bool beam_box(const Beam& B, float4 lo, float4 hi) {
     return sn <= sf;
 }
 
+#ifndef VPL_BRANCHLESS_NODE
+#define VPL_BRANCHLESS_NODE 1   // branch-free node loads and leaf tests in the beam traversal (C4: -4%)
+#endif
+#ifndef VPL_LEAF_SEG1
+#define VPL_LEAF_SEG1 0     // 1: leaf tests through mt_seg1 (no mask branch) instead of mt_segs
+#endif
+#ifndef VPL_BRANCHLESS2
+#define VPL_BRANCHLESS2 0   // 1: branch-free single-VPL segment setup and cache tests (kGroup == 1)
+#endif
 #ifndef VPL_MT_EARLY
 #define VPL_MT_EARLY 0      // 1: skip the second half of MT when no active lane's u lies in [0, 1]
 #endif
@@ -164,6 +173,21 @@ __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, 
     }
 #endif
     return hit;
+}
+
+// exact MT (O9) of one segment, no branches (single-segment paths)
+__device__ __forceinline__ bool mt_seg1(f3 o, f3 d, float tmin, float tmax, float4 a, float4 b, float4 c) {
+    const f3 v0 = xyz(a), e1 = xyz(b), e2 = xyz(c);
+    const f3 pv = cross(d, e2);
+    const float det = dot(e1, pv);
+    const float inv = 1.0f / det;
+    const f3 s = o - v0;
+    const float u = dot(s, pv) * inv;
+    const f3 q = cross(s, e1);
+    const float v = dot(d, q) * inv;
+    const float t = dot(e2, q) * inv;
+    // (det == 0 needs no test of its own: u is then NaN or +-inf and fails u >= 0 or u <= 1)
+    return (u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) & (t > tmin) & (t < tmax);
 }
 
 template <bool kCount>
@@ -327,6 +351,15 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
         const int node = idx >= 0 ? sstack[idx] : -1;
         if (kCount && lane == 0) { st->wsteps += 1; st->cones += sp >= 2 ? 2 * kWide : kWide; }
         sp = max(sp - 2, 0);
+#if VPL_BRANCHLESS_NODE
+        // no branch: an empty half-step loads the root's children (cached) and masks the result
+        const int nsafe = node >= 0 ? node : 0;
+        const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)nsafe << 9) + ((lane & (kWide - 1)) << 5));
+        const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
+        int ref = node >= 0 ? __float_as_int(lo.w) : INT_MIN;
+        const int axis = __float_as_int(hi.w);
+        const bool hit = (ref != INT_MIN) & beam_box(B, lo, hi);
+#else
         bool hit = false;
         int ref = INT_MIN, axis = 0;
         if (node >= 0) {
@@ -340,6 +373,7 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
             hit = ref != INT_MIN && beam_box(B, lo, hi);
 #endif
         }
+#endif
         const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
         unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
         if (Bi) {
@@ -360,7 +394,23 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
             const int k = __ffs(Bl) - 1;
             Bl &= Bl - 1u;
             const int tri = ~__shfl_sync(0xFFFFFFFFu, ref, k) >> 3;
+#if VPL_BRANCHLESS_NODE
+            {   // every lane runs the test (the warp would anyway); lanes with nothing pending mask it off
+                const float4* tr = bv.tris + 3 * tri;
+#if VPL_GROUP == 1 && VPL_LEAF_SEG1
+                if (kCount) st->tris += S.pend & 1u;
+                const unsigned h = (S.pend & 1u) &
+                                   (unsigned)mt_seg1(x, S.d[0], tmin, S.tmax[0], __ldg(tr), __ldg(tr + 1), __ldg(tr + 2));
+#else
+                const unsigned h = mt_segs<kCount>(x, S, S.pend, tmin, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), st);
+#endif
+                S.occ |= h;
+                S.pend &= ~h;
+                if (h) cache.found(tri);
+            }
+#else
             test_tri<kCount>(bv, x, S, tmin, tri, cache, st);
+#endif
             if (!__any_sync(0xFFFFFFFFu, S.pend != 0)) return;
         }
     }
@@ -451,6 +501,47 @@ __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_rec
     Segs S;
     S.pend = 0; S.occ = 0;
     unsigned traced = 0;
+#if VPL_BRANCHLESS2 && VPL_GROUP == 1
+    {
+        // single VPL, branch-free: cull (exact O13), then segment setup and cache tests for the
+        // whole warp behind warp-uniform votes, every per-lane decision a mask
+        const float4 nb = __ldg((const float4*)(vpls + i) + 1);
+        const int tri_i = __float_as_int(__ldg((const float*)(vpls + i) + 3));
+        const f3 d = yk[0] - x;
+        const float r2 = dot(d, d);
+        const float cx = dot(nx, d);
+        const float ci = -dot(xyz(nb), d);
+        const bool tr = active && tri_i != tri_x && cx > 0.0f && ci > 0.0f;
+        *vis = 0;
+        w[0] = 0.0f;
+        if (!__any_sync(0xFFFFFFFFu, tr)) return 0;
+        traced = tr ? 1u : 0u;
+        w[0] = tr ? __fdividef(cx * ci, r2 * fmaxf(r2, b2)) : 0.0f;
+        const float dist = sqrtf(r2);   // = sqrtf(dot(d, d)) of O9's segment setup
+        S.d[0] = mk3(d.x / dist, d.y / dist, d.z / dist);
+        S.tmax[0] = dist - eps;
+        S.pend = (tr && S.tmax[0] > eps) ? 1u : 0u;
+        const uint32_t t0 = kCount ? st->tris : 0;
+        unsigned cp = cache.vis_streak ? 0u : S.pend;   // VPL_CACHE_STREAK
+        const int slots[3] = {cache.own0, VPL_CACHE_OWN2 ? cache.own1 : -1,
+                              (VPL_CACHE_WARP && cache.warp != cache.own0 && cache.warp != cache.own1) ? cache.warp : -1};
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const bool need = cp && slots[q] >= 0;
+            if (__any_sync(0xFFFFFFFFu, need)) {
+                const float4* tp = bv.tris + 3 * (need ? slots[q] : 0);
+                if (kCount) st->tris += need ? 1u : 0u;
+                const bool h = need && mt_seg1(x, S.d[0], eps, S.tmax[0], __ldg(tp), __ldg(tp + 1), __ldg(tp + 2));
+                if (h) { S.occ = 1u; S.pend = 0u; cp = 0u; cache.found(slots[q]); }
+            }
+        }
+        if (kCount) { st->chits += __popc(S.occ); st->ctests += st->tris - t0; }
+        resolve_group<kCount>(bv, x, S, eps, yk, g, cache, sstack, st);
+        *vis = traced & ~S.occ;
+        if (traced) cache.vis_streak = (*vis == traced);
+        return traced;
+    }
+#endif
 #pragma unroll
     for (int k = 0; k < kGroup; ++k) {
         w[k] = 0.0f;

@@ -156,6 +156,16 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                     const unsigned tr = shade_group<kCount>(bv, vpls, i, gsz, yk, x, nxv, trv, active, eps, b2, cache,
                                                             sstack, &st, &vis, w);
                     if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
+#if VPL_BRANCHLESS2 && VPL_GROUP == 1
+                    if (__any_sync(0xFFFFFFFFu, vis != 0)) {
+                        // fmaf(phi, 0, part) == part bitwise (phi finite, >= 0), so no per-lane branch
+                        const float4 phi = __ldg((const float4*)(vpls + i) + 2);
+                        const float ww = (vis & 1u) ? w[0] : 0.0f;
+                        part[0] = fmaf(phi.x, ww, part[0]);
+                        part[1] = fmaf(phi.y, ww, part[1]);
+                        part[2] = fmaf(phi.z, ww, part[2]);
+                    }
+#else
 #pragma unroll
                     for (int k = 0; k < kGroup; ++k) {
                         if (vis & (1u << k)) {
@@ -165,6 +175,7 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                             part[2] = fmaf(phi.z, w[k], part[2]);
                         }
                     }
+#endif
                     i += gsz;
                 }
                 s_acc[0][lane] += part[0]; s_acc[1][lane] += part[1]; s_acc[2][lane] += part[2];
