@@ -33,9 +33,6 @@ namespace vplgi {
 #ifndef VPL_GROUP
 #define VPL_GROUP 1
 #endif
-#ifndef VPL_QUAD
-#define VPL_QUAD 0          // 1: four nodes per traversal step (two children per lane)
-#endif
 #ifndef VPL_NO_ORDER
 #define VPL_NO_ORDER 0      // 1: push hit children in lane order (no near-to-far ordering)
 #endif
@@ -83,39 +80,6 @@ __device__ __forceinline__ bool beam_box(const Beam& B, float4 lo, float4 hi) {
     return sn <= sf;
 }
 
-#ifndef VPL_BRANCHLESS_NODE
-#define VPL_BRANCHLESS_NODE 1   // branch-free node loads and leaf tests in the beam traversal (C4: -4%)
-#endif
-#ifndef VPL_LEAF_SEG1
-#define VPL_LEAF_SEG1 0     // 1: leaf tests through mt_seg1 (no mask branch) instead of mt_segs
-#endif
-#ifndef VPL_BRANCHLESS2
-#define VPL_BRANCHLESS2 0   // 1: branch-free single-VPL segment setup and cache tests (kGroup == 1)
-#endif
-#ifndef VPL_MT_EARLY
-#define VPL_MT_EARLY 0      // 1: skip the second half of MT when no active lane's u lies in [0, 1]
-#endif
-#ifndef VPL_BEAM_SMEM
-#define VPL_BEAM_SMEM 0     // 1: keep the beam coefficients in shared memory (frees ~15 registers)
-#endif
-// warp-uniform beam in shared memory: F0 = (a0, s_lo), F1 = (b0, s_hi), F2 = (a1, pos bits), F3 = (b1, 0)
-__device__ __forceinline__ float4 lds4(unsigned a) {
-    float4 r;
-    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(a));
-    return r;
-}
-__device__ __forceinline__ bool beam_box_s(unsigned sb, float4 lo, float4 hi) {
-    const float4 F0 = lds4(sb), F1 = lds4(sb + 16), F2 = lds4(sb + 32), F3 = lds4(sb + 48);
-    const unsigned pos = __float_as_uint(F2.w);
-    const bool px = pos & 1u, py = pos & 2u, pz = pos & 4u;
-    float s0x = fmaf(px ? lo.x : hi.x, F0.x, -F1.x), s1x = fmaf(px ? hi.x : lo.x, F2.x, -F3.x);
-    float s0y = fmaf(py ? lo.y : hi.y, F0.y, -F1.y), s1y = fmaf(py ? hi.y : lo.y, F2.y, -F3.y);
-    float s0z = fmaf(pz ? lo.z : hi.z, F0.z, -F1.z), s1z = fmaf(pz ? hi.z : lo.z, F2.z, -F3.z);
-    float sn = fmax3(s0x, s0y, fmaxf(s0z, F0.w));
-    float sf = fmin3(s1x, s1y, fminf(s1z, F1.w));
-    return sn <= sf;
-}
-
 // One lane's shadow segments of a group: origin x (the receiver), direction
 // d_k = (y_k - x)/|y_k - x|, t in (eps, |y_k - x| - eps)  (O9).
 struct Segs {
@@ -134,25 +98,6 @@ __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, 
     const f3 v0 = xyz(a), e1 = xyz(b), e2 = xyz(c);
     const f3 s = o - v0;
     unsigned hit = 0;
-#if VPL_MT_EARLY && VPL_GROUP == 1
-    // single segment: u first; the rest of O9 only if some active lane's u is in [0, 1]
-    if (mask & 1u) {
-        if (kCount) st->tris += 1;
-        const f3 d = S.d[0];
-        const f3 pv = cross(d, e2);
-        const float det = dot(e1, pv);
-        const float inv = 1.0f / det;
-        const float u = dot(s, pv) * inv;
-        // (det == 0 needs no test of its own: u is then NaN or +-inf and fails u >= 0 or u <= 1)
-        const bool uok = (u >= 0.0f) & (u <= 1.0f);
-        if (__any_sync(__activemask(), uok)) {
-            const f3 q = cross(s, e1);
-            const float v = dot(d, q) * inv;
-            const float t = dot(e2, q) * inv;
-            if (uok & (v >= 0.0f) & ((u + v) <= 1.0f) & (t > tmin) & (t < S.tmax[0])) hit = 1u;
-        }
-    }
-#else
     const f3 q = cross(s, e1);
     const float tq = dot(e2, q);
 #pragma unroll
@@ -171,23 +116,7 @@ __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, 
                 hit |= 1u << k;
         }
     }
-#endif
     return hit;
-}
-
-// exact MT (O9) of one segment, no branches (single-segment paths)
-__device__ __forceinline__ bool mt_seg1(f3 o, f3 d, float tmin, float tmax, float4 a, float4 b, float4 c) {
-    const f3 v0 = xyz(a), e1 = xyz(b), e2 = xyz(c);
-    const f3 pv = cross(d, e2);
-    const float det = dot(e1, pv);
-    const float inv = 1.0f / det;
-    const f3 s = o - v0;
-    const float u = dot(s, pv) * inv;
-    const f3 q = cross(s, e1);
-    const float v = dot(d, q) * inv;
-    const float t = dot(e2, q) * inv;
-    // (det == 0 needs no test of its own: u is then NaN or +-inf and fails u >= 0 or u <= 1)
-    return (u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) & (t > tmin) & (t < tmax);
 }
 
 template <bool kCount>
@@ -273,85 +202,16 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
         test_tri<kCount>(bv, x, S, tmin, 0, cache, st);
         return;
     }
-#if VPL_BEAM_SMEM
-    const unsigned sbeam = (unsigned)__cvta_generic_to_shared(sstack + kWarpStack);
-    if (lane == 0) {
-        float4* F = (float4*)(sstack + kWarpStack);
-        F[0] = make_float4(B.a0[0], B.a0[1], B.a0[2], B.s_lo);
-        F[1] = make_float4(B.b0[0], B.b0[1], B.b0[2], B.s_hi);
-        F[2] = make_float4(B.a1[0], B.a1[1], B.a1[2], __uint_as_float(B.pos));
-        F[3] = make_float4(B.b1[0], B.b1[1], B.b1[2], 0.0f);
-    }
-#endif
     // the stack holds inner nodes only
     if (lane == 0) sstack[0] = bv.root;
     __syncwarp();
     int sp = 1;
-#if VPL_QUAD
-    // each step pops the top four: lanes 0-15 test the children of the 1st and 3rd entries,
-    // lanes 16-31 those of the 2nd and 4th (two children per lane)
-    while (sp > 0) {
-        const int i1 = sp - 1 - half, i2 = sp - 3 - half;
-        const int n1 = i1 >= 0 ? sstack[i1] : -1;
-        const int n2 = i2 >= 0 ? sstack[i2] : -1;
-        if (kCount && lane == 0) { st->wsteps += 1; st->cones += (sp >= 4 ? 4 : sp) * kWide; }
-        sp = max(sp - 4, 0);
-        const int coff = (lane & (kWide - 1)) << 5;
-        bool h1 = false, h2 = false;
-        int r1 = INT_MIN, a1 = 0, r2 = INT_MIN, a2 = 0;
-        if (n1 >= 0) {
-            const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)n1 << 9) + coff);
-            const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
-            r1 = __float_as_int(lo.w); a1 = __float_as_int(hi.w);
-            h1 = r1 != INT_MIN && beam_box(B, lo, hi);
-        }
-        if (n2 >= 0) {
-            const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)n2 << 9) + coff);
-            const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
-            r2 = __float_as_int(lo.w); a2 = __float_as_int(hi.w);
-            h2 = r2 != INT_MIN && beam_box(B, lo, hi);
-        }
-        const unsigned Bi1 = __ballot_sync(0xFFFFFFFFu, h1 && r1 >= 0);
-        const unsigned Bi2 = __ballot_sync(0xFFFFFFFFu, h2 && r2 >= 0);
-        unsigned Bl1 = __ballot_sync(0xFFFFFFFFu, h1 && r1 < 0);
-        unsigned Bl2 = __ballot_sync(0xFFFFFFFFu, h2 && r2 < 0);
-        if (Bi1 | Bi2) {
-            const int nA = __popc(Bi1 & 0xFFFFu), nB = __popc(Bi1 >> 16);
-            const int nC = __popc(Bi2 & 0xFFFFu), nD = __popc(Bi2 >> 16);
-            // bottom -> top: D, C, B, A (A = the old top is visited first)
-            const int base1 = sp + nD + nC + (half ? 0 : nB);
-            const int base2 = sp + (half ? 0 : nD);
-            if (h1 && r1 >= 0) {
-                const int nh = half ? nB : nA, rank = __popc(Bi1 & below & hmask);
-                const bool rev = (dir_neg >> a1) & 1u;
-                sstack[base1 + (rev ? rank : nh - 1 - rank)] = r1;
-            }
-            if (h2 && r2 >= 0) {
-                const int nh = half ? nD : nC, rank = __popc(Bi2 & below & hmask);
-                const bool rev = (dir_neg >> a2) & 1u;
-                sstack[base2 + (rev ? rank : nh - 1 - rank)] = r2;
-            }
-            sp += nA + nB + nC + nD;
-        }
-        __syncwarp();
-        while (Bl1 | Bl2) {   // hit triangle children
-            const bool first = Bl1 != 0;
-            const unsigned m = first ? Bl1 : Bl2;
-            const int k = __ffs(m) - 1;
-            if (first) Bl1 &= Bl1 - 1u; else Bl2 &= Bl2 - 1u;
-            const int tri = ~__shfl_sync(0xFFFFFFFFu, first ? r1 : r2, k) >> 3;
-            test_tri<kCount>(bv, x, S, tmin, tri, cache, st);
-            if (!__any_sync(0xFFFFFFFFu, S.pend != 0)) return;
-        }
-    }
-#else
     // each step pops the top two (lanes 0-15 take the top one)
     while (sp > 0) {
         const int idx = sp - 1 - half;
         const int node = idx >= 0 ? sstack[idx] : -1;
         if (kCount && lane == 0) { st->wsteps += 1; st->cones += sp >= 2 ? 2 * kWide : kWide; }
         sp = max(sp - 2, 0);
-#if VPL_BRANCHLESS_NODE
         // no branch: an empty half-step loads the root's children (cached) and masks the result
         const int nsafe = node >= 0 ? node : 0;
         const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)nsafe << 9) + ((lane & (kWide - 1)) << 5));
@@ -359,21 +219,6 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
         int ref = node >= 0 ? __float_as_int(lo.w) : INT_MIN;
         const int axis = __float_as_int(hi.w);
         const bool hit = (ref != INT_MIN) & beam_box(B, lo, hi);
-#else
-        bool hit = false;
-        int ref = INT_MIN, axis = 0;
-        if (node >= 0) {
-            const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)node << 9) + ((lane & (kWide - 1)) << 5));
-            const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
-            ref = __float_as_int(lo.w);
-            axis = __float_as_int(hi.w);
-#if VPL_BEAM_SMEM
-            hit = ref != INT_MIN && beam_box_s(sbeam, lo, hi);
-#else
-            hit = ref != INT_MIN && beam_box(B, lo, hi);
-#endif
-        }
-#endif
         const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
         unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
         if (Bi) {
@@ -394,27 +239,16 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
             const int k = __ffs(Bl) - 1;
             Bl &= Bl - 1u;
             const int tri = ~__shfl_sync(0xFFFFFFFFu, ref, k) >> 3;
-#if VPL_BRANCHLESS_NODE
-            {   // every lane runs the test (the warp would anyway); lanes with nothing pending mask it off
+            {   // no branch around the test: lanes with nothing pending are masked inside mt_segs
                 const float4* tr = bv.tris + 3 * tri;
-#if VPL_GROUP == 1 && VPL_LEAF_SEG1
-                if (kCount) st->tris += S.pend & 1u;
-                const unsigned h = (S.pend & 1u) &
-                                   (unsigned)mt_seg1(x, S.d[0], tmin, S.tmax[0], __ldg(tr), __ldg(tr + 1), __ldg(tr + 2));
-#else
                 const unsigned h = mt_segs<kCount>(x, S, S.pend, tmin, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), st);
-#endif
                 S.occ |= h;
                 S.pend &= ~h;
                 if (h) cache.found(tri);
             }
-#else
-            test_tri<kCount>(bv, x, S, tmin, tri, cache, st);
-#endif
             if (!__any_sync(0xFFFFFFFFu, S.pend != 0)) return;
         }
     }
-#endif
 }
 
 // Resolve the pending segments of a group: beam over the group, else one beam
@@ -501,47 +335,6 @@ __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_rec
     Segs S;
     S.pend = 0; S.occ = 0;
     unsigned traced = 0;
-#if VPL_BRANCHLESS2 && VPL_GROUP == 1
-    {
-        // single VPL, branch-free: cull (exact O13), then segment setup and cache tests for the
-        // whole warp behind warp-uniform votes, every per-lane decision a mask
-        const float4 nb = __ldg((const float4*)(vpls + i) + 1);
-        const int tri_i = __float_as_int(__ldg((const float*)(vpls + i) + 3));
-        const f3 d = yk[0] - x;
-        const float r2 = dot(d, d);
-        const float cx = dot(nx, d);
-        const float ci = -dot(xyz(nb), d);
-        const bool tr = active && tri_i != tri_x && cx > 0.0f && ci > 0.0f;
-        *vis = 0;
-        w[0] = 0.0f;
-        if (!__any_sync(0xFFFFFFFFu, tr)) return 0;
-        traced = tr ? 1u : 0u;
-        w[0] = tr ? __fdividef(cx * ci, r2 * fmaxf(r2, b2)) : 0.0f;
-        const float dist = sqrtf(r2);   // = sqrtf(dot(d, d)) of O9's segment setup
-        S.d[0] = mk3(d.x / dist, d.y / dist, d.z / dist);
-        S.tmax[0] = dist - eps;
-        S.pend = (tr && S.tmax[0] > eps) ? 1u : 0u;
-        const uint32_t t0 = kCount ? st->tris : 0;
-        unsigned cp = cache.vis_streak ? 0u : S.pend;   // VPL_CACHE_STREAK
-        const int slots[3] = {cache.own0, VPL_CACHE_OWN2 ? cache.own1 : -1,
-                              (VPL_CACHE_WARP && cache.warp != cache.own0 && cache.warp != cache.own1) ? cache.warp : -1};
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            const bool need = cp && slots[q] >= 0;
-            if (__any_sync(0xFFFFFFFFu, need)) {
-                const float4* tp = bv.tris + 3 * (need ? slots[q] : 0);
-                if (kCount) st->tris += need ? 1u : 0u;
-                const bool h = need && mt_seg1(x, S.d[0], eps, S.tmax[0], __ldg(tp), __ldg(tp + 1), __ldg(tp + 2));
-                if (h) { S.occ = 1u; S.pend = 0u; cp = 0u; cache.found(slots[q]); }
-            }
-        }
-        if (kCount) { st->chits += __popc(S.occ); st->ctests += st->tris - t0; }
-        resolve_group<kCount>(bv, x, S, eps, yk, g, cache, sstack, st);
-        *vis = traced & ~S.occ;
-        if (traced) cache.vis_streak = (*vis == traced);
-        return traced;
-    }
-#endif
 #pragma unroll
     for (int k = 0; k < kGroup; ++k) {
         w[k] = 0.0f;

@@ -74,9 +74,6 @@ __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, floa
 // One warp per CTA: the traversal stack is then at a fixed shared-memory
 // address (no per-warp base to keep live in a register), and 32 one-warp
 // CTAs fill an SM at the 64-register budget.
-#ifndef VPL_NX_SMEM
-#define VPL_NX_SMEM 0   // 1: keep the receiver normal / triangle in shared memory (fewer live registers)
-#endif
 #ifndef VPL_CLUSTER_CULL
 #define VPL_CLUSTER_CULL 1   // skip 32-VPL clusters no lane of the warp can trace
 #endif
@@ -88,12 +85,8 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                                                 const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
                                                 vpl_counters* __restrict__ ctr, int* __restrict__ queue,
                                                 const float4* __restrict__ clusters) {
-    __shared__ __align__(16) int sstack[kWarpStack + 16];   // traversal stack + the warp's beam (VPL_BEAM_SMEM)
+    __shared__ int sstack[kWarpStack];
     __shared__ float s_acc[3][32];   // running per-lane totals (kept out of the register budget)
-#if VPL_NX_SMEM
-    __shared__ __align__(16) float4 s_nx[32];
-    const unsigned s_nx_addr = (unsigned)__cvta_generic_to_shared(&s_nx[threadIdx.x]);
-#endif
     const int lane = threadIdx.x;
     const int64_t nw = tm.n_warps();
     const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
@@ -113,10 +106,6 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             active = tri_x >= 0 && __float_as_int(b.w) != 0;
             x = xyz(a); nx = xyz(b);
         }
-#if VPL_NX_SMEM
-        s_nx[lane] = make_float4(nx.x, nx.y, nx.z, __int_as_float(tri_x));
-        __syncwarp();
-#endif
         s_acc[0][lane] = 0.0f; s_acc[1][lane] = 0.0f; s_acc[2][lane] = 0.0f;
         OccluderCache cache;
         TravStats st;
@@ -129,54 +118,30 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             for (int i0 = 0; i0 < M; i0 += 256) {
                 float part[3] = {0.0f, 0.0f, 0.0f};
                 const int i1 = min(M, i0 + 256);
-                for (int i = i0; i < i1;) {
-#if VPL_NX_SMEM
-                    if (clusters && (i & (kCluster - 1)) == 0 &&
-                        !__any_sync(0xFFFFFFFFu, active && cluster_may_trace(clusters + 4 * (i / kCluster), x,
-                                                                             xyz(lds4(s_nx_addr))))) {
-#else
-                    if (clusters && (i & (kCluster - 1)) == 0 &&
-                        !__any_sync(0xFFFFFFFFu, active && cluster_may_trace(clusters + 4 * (i / kCluster), x, nx))) {
-#endif
-                        i = min(i + kCluster, i1);     // no lane can trace any VPL of this cluster
-                        continue;
-                    }
-                    f3 yk[kGroup];
-                    const int gsz = group_at(vpls, i, i1, xr, yk);
-                    unsigned vis;
-                    float w[kGroup];
-#if VPL_NX_SMEM
-                    const float4 nt = lds4(s_nx_addr);   // receiver normal + triangle, re-read per VPL (registers)
-                    const f3 nxv = xyz(nt);
-                    const int trv = __float_as_int(nt.w);
-#else
-                    const f3 nxv = nx;
-                    const int trv = tri_x;
-#endif
-                    const unsigned tr = shade_group<kCount>(bv, vpls, i, gsz, yk, x, nxv, trv, active, eps, b2, cache,
-                                                            sstack, &st, &vis, w);
-                    if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
-#if VPL_BRANCHLESS2 && VPL_GROUP == 1
-                    if (__any_sync(0xFFFFFFFFu, vis != 0)) {
-                        // fmaf(phi, 0, part) == part bitwise (phi finite, >= 0), so no per-lane branch
-                        const float4 phi = __ldg((const float4*)(vpls + i) + 2);
-                        const float ww = (vis & 1u) ? w[0] : 0.0f;
-                        part[0] = fmaf(phi.x, ww, part[0]);
-                        part[1] = fmaf(phi.y, ww, part[1]);
-                        part[2] = fmaf(phi.z, ww, part[2]);
-                    }
-#else
+                for (int c0 = i0; c0 < i1; c0 += kCluster) {       // clusters of 32 VPLs (i0 % 32 == 0)
+                    if (clusters &&
+                        !__any_sync(0xFFFFFFFFu, active && cluster_may_trace(clusters + 4 * (c0 / kCluster), x, nx)))
+                        continue;                                      // no lane can trace any VPL of it
+                    const int c1 = min(c0 + kCluster, i1);
+                    for (int i = c0; i < c1;) {
+                        f3 yk[kGroup];
+                        const int gsz = group_at(vpls, i, c1, xr, yk);
+                        unsigned vis;
+                        float w[kGroup];
+                        const unsigned tr = shade_group<kCount>(bv, vpls, i, gsz, yk, x, nx, tri_x, active, eps, b2,
+                                                                cache, sstack, &st, &vis, w);
+                        if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
 #pragma unroll
-                    for (int k = 0; k < kGroup; ++k) {
-                        if (vis & (1u << k)) {
-                            const float4 phi = __ldg((const float4*)(vpls + i + k) + 2);
-                            part[0] = fmaf(phi.x, w[k], part[0]);
-                            part[1] = fmaf(phi.y, w[k], part[1]);
-                            part[2] = fmaf(phi.z, w[k], part[2]);
+                        for (int k = 0; k < kGroup; ++k) {
+                            if (vis & (1u << k)) {
+                                const float4 phi = __ldg((const float4*)(vpls + i + k) + 2);
+                                part[0] = fmaf(phi.x, w[k], part[0]);
+                                part[1] = fmaf(phi.y, w[k], part[1]);
+                                part[2] = fmaf(phi.z, w[k], part[2]);
+                            }
                         }
+                        i += gsz;
                     }
-#endif
-                    i += gsz;
                 }
                 s_acc[0][lane] += part[0]; s_acc[1][lane] += part[1]; s_acc[2][lane] += part[2];
             }
@@ -208,7 +173,7 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
 __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict__ gb, const vpl_record* __restrict__ vpls,
                           int32_t M, const int32_t* __restrict__ pixels, int32_t n_px, uint32_t* __restrict__ tbits,
                           uint32_t* __restrict__ vbits) {
-    __shared__ __align__(16) int s_stack[2][kWarpStack + 16];
+    __shared__ int s_stack[2][kWarpStack];
     int* sstack = s_stack[threadIdx.x >> 5];
     int64_t words = (M + 31) / 32;
     OccluderCache cache;
