@@ -270,7 +270,7 @@ __device__ __forceinline__ void resolve_group(const BvhView& bv, f3 x, Segs& S, 
         beam_traverse<kCount>(bv, x, S, eps, B, B.pos, cache, sstack, st);
     } else {
         // loose: one beam per VPL of the group, loose single beams go per ray
-        const bool several = __popc(kany) > 1;
+        const bool several = kGroup > 1 && __popc(kany) > 1;   // compile-time false for single-VPL groups
         const unsigned all = S.pend;
 #pragma unroll
         for (int k = 0; k < kGroup; ++k) {
