@@ -84,18 +84,23 @@ template <bool kCount>
 __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb,
                                                 const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
                                                 vpl_counters* __restrict__ ctr, int* __restrict__ queue,
-                                                const float4* __restrict__ clusters) {
+                                                const float4* __restrict__ clusters, int32_t chunk, int32_t n_chunks,
+                                                float* __restrict__ part_out, int64_t npix) {
     __shared__ int sstack[kWarpStack];
     __shared__ float s_acc[3][32];   // running per-lane totals (kept out of the register budget)
     const int lane = threadIdx.x;
-    const int64_t nw = tm.n_warps();
+    const int64_t ntask = tm.n_warps() * n_chunks;
     const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
     while (true) {
         int64_t g;
         if (lane == 0) g = atomicAdd(queue, 1);
         g = __shfl_sync(0xFFFFFFFFu, g, 0);
-        if (g >= nw) break;
-        int32_t pix = tm.pixel(g, lane);
+        if (g >= ntask) break;
+        // task = (8x4 pixel block, VPL chunk): fine-grained enough that the dynamic queue balances
+        // the SMs even when a rank holds 1/8 of the frame
+        const int ch = (int)(g % n_chunks);
+        const int vbeg = ch * chunk, vend = min(M, vbeg + chunk);
+        int32_t pix = tm.pixel(g / n_chunks, lane);
         bool active = false;
         f3 x = mk3(0, 0, 0), nx = mk3(0, 0, 0);
         int tri_x = -1;
@@ -115,9 +120,9 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             const int l0 = __ffs(am) - 1;
             const f3 xr = mk3(__shfl_sync(0xFFFFFFFFu, x.x, l0), __shfl_sync(0xFFFFFFFFu, x.y, l0),
                               __shfl_sync(0xFFFFFFFFu, x.z, l0));
-            for (int i0 = 0; i0 < M; i0 += 256) {
+            for (int i0 = vbeg; i0 < vend; i0 += 256) {
                 float part[3] = {0.0f, 0.0f, 0.0f};
-                const int i1 = min(M, i0 + 256);
+                const int i1 = min(vend, i0 + 256);
                 for (int c0 = i0; c0 < i1; c0 += kCluster) {       // clusters of 32 VPLs (i0 % 32 == 0)
                     if (clusters &&
                         !__any_sync(0xFFFFFFFFu, active && cluster_may_trace(clusters + 4 * (c0 / kCluster), x, nx)))
@@ -147,15 +152,20 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             }
         }
         if (pix >= 0) {
-            const float s = (float)(1.0 / kPiR);
-            f3 rho = xyz(((const float4*)(gb + pix))[2]);
-            float* o = rgb + 3 * (int64_t)pix;
-            o[0] = active ? s_acc[0][lane] * rho.x * s : 0.0f;
-            o[1] = active ? s_acc[1][lane] * rho.y * s : 0.0f;
-            o[2] = active ? s_acc[2][lane] * rho.z * s : 0.0f;
+            if (n_chunks == 1) {
+                const float s = (float)(1.0 / kPiR);
+                f3 rho = xyz(((const float4*)(gb + pix))[2]);
+                float* o = rgb + 3 * (int64_t)pix;
+                o[0] = active ? s_acc[0][lane] * rho.x * s : 0.0f;
+                o[1] = active ? s_acc[1][lane] * rho.y * s : 0.0f;
+                o[2] = active ? s_acc[2][lane] * rho.z * s : 0.0f;
+            } else {   // chunk partial sums, folded in chunk order by k_gather_finish
+                float* o = part_out + 3 * ((int64_t)ch * npix + pix);
+                o[0] = s_acc[0][lane]; o[1] = s_acc[1][lane]; o[2] = s_acc[2][lane];
+            }
         }
         if (kCount) {
-            unsigned long long pairs = active ? (unsigned long long)M : 0ull;
+            unsigned long long pairs = active ? (unsigned long long)(vend - vbeg) : 0ull;
             unsigned long long v[12] = {pairs, n_traced, n_vis, st.boxes, st.tris, st.wrays, st.wsteps,
                                         st.cones, st.cpk, st.rpk, st.chits, st.ctests};
 #pragma unroll
@@ -363,19 +373,64 @@ __global__ void k_image_err_final(const double* __restrict__ part, int nb, doubl
     out[threadIdx.x] = t;
 }
 
+// fold the VPL-chunk partial sums of every listed pixel in chunk order (fp32),
+// then Eq. 1's rho/pi (O13); miss / back-face pixels get 0
+__global__ void k_gather_finish(TileMap tm, const vpl_gpoint* __restrict__ gb, const float* __restrict__ part,
+                                int32_t n_chunks, int64_t npix, float* __restrict__ rgb) {
+    int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (g >= tm.n_warps()) return;
+    int32_t pix = tm.pixel(g, lane);
+    if (pix < 0) return;
+    const float4* gp = (const float4*)(gb + pix);
+    const float4 a = gp[0], b = gp[1], c = gp[2];
+    const bool active = __float_as_int(a.w) >= 0 && __float_as_int(b.w) != 0;
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+    for (int ch = 0; ch < n_chunks; ++ch) {
+        const float* p = part + 3 * ((int64_t)ch * npix + pix);
+        acc[0] += p[0]; acc[1] += p[1]; acc[2] += p[2];
+    }
+    const float s = (float)(1.0 / kPiR);
+    float* o = rgb + 3 * (int64_t)pix;
+    o[0] = active ? acc[0] * c.x * s : 0.0f;
+    o[1] = active ? acc[1] * c.y * s : 0.0f;
+    o[2] = active ? acc[2] * c.z * s : 0.0f;
+}
+
+// VPL chunking of the gather's work items: depends on M only (so any tile split
+// reproduces the same sums): chunk = max(CHUNK_MIN, ceil(M / CHUNKS) rounded up to 256); 128 chunks
+// put the C4 load-balance efficiency at 8 ranks at 95% (tools/shard_sim.py)
+#ifndef VPL_GATHER_CHUNKS
+#define VPL_GATHER_CHUNKS 128
+#endif
+#ifndef VPL_GATHER_CHUNK_MIN
+#define VPL_GATHER_CHUNK_MIN 256
+#endif
+static inline void gather_chunks(int32_t M, int32_t* chunk, int32_t* n_chunks) {
+    int64_t c = ((int64_t)M + VPL_GATHER_CHUNKS - 1) / VPL_GATHER_CHUNKS;
+    c = (c + 255) / 256 * 256;
+    if (c < VPL_GATHER_CHUNK_MIN) c = VPL_GATHER_CHUNK_MIN;
+    *chunk = (int32_t)c;
+    *n_chunks = M > 0 ? (int32_t)(((int64_t)M + c - 1) / c) : 1;
+}
+
 struct GatherWork {
     int* queue;
     unsigned* box;
     float4* clusters;
+    float* part;
     uint32_t *keys, *keys2;
     int32_t *idx, *idx2;
     vpl_record* sorted;
     void* cub;
     size_t cub_bytes;
 };
-static size_t gather_layout(int32_t M, char* base, GatherWork* w) {
+static size_t gather_layout(int32_t M, int64_t npix, char* base, GatherWork* w) {
     Bump b{base};
     w->queue = b.take<int>(1);
+    int32_t chunk, nch;
+    gather_chunks(M, &chunk, &nch);
+    w->part = b.take<float>(nch > 1 ? (size_t)nch * (size_t)npix * 3 : 1);
     w->box = b.take<unsigned>(6);
     size_t m = (size_t)(M > 0 ? M : 1);
     w->keys = b.take<uint32_t>(m);
@@ -429,10 +484,10 @@ int32_t vpl_render_gbuffer(const void* d_scene, const void* d_bvh, const int32_t
     return VPL_OK;
 }
 
-int32_t vpl_gather_bytes(int32_t n_vpls, size_t* work_bytes) {
-    if (!work_bytes || n_vpls < 0) return VPL_EINVAL;
+int32_t vpl_gather_bytes(int32_t n_vpls, int64_t n_pixels, size_t* work_bytes) {
+    if (!work_bytes || n_vpls < 0 || n_pixels < 0) return VPL_EINVAL;
     GatherWork w;
-    *work_bytes = gather_layout(n_vpls, nullptr, &w);
+    *work_bytes = gather_layout(n_vpls, n_pixels, nullptr, &w);
     return VPL_OK;
 }
 
@@ -443,15 +498,18 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
         set_error("vpl_gather_indirect: bad arguments");
         return VPL_EINVAL;
     }
-    GatherWork w;
-    if (work_bytes < gather_layout(n_vpls, nullptr, &w)) {
-        set_error("vpl_gather_indirect: work buffer smaller than vpl_gather_bytes(n_vpls)");
-        return VPL_ESMALL;
-    }
-    gather_layout(n_vpls, (char*)d_work, &w);
     cudaStream_t s = (cudaStream_t)stream;
     SceneHdr hh;
     VPL_TRY(read_scene_hdr(d_scene, s, &hh));
+    GatherWork w;
+    const int64_t npix = (int64_t)hh.W * hh.H;
+    if (work_bytes < gather_layout(n_vpls, npix, nullptr, &w)) {
+        set_error("vpl_gather_indirect: work buffer smaller than vpl_gather_bytes(n_vpls, W*H)");
+        return VPL_ESMALL;
+    }
+    gather_layout(n_vpls, npix, (char*)d_work, &w);
+    int32_t chunk, n_chunks;
+    gather_chunks(n_vpls, &chunk, &n_chunks);
     TileMap tm;
     VPL_TRY(make_tilemap(hh, d_tiles, n_tiles, tile_w, tile_h, &tm));
     if (n_tiles == 0) return VPL_OK;
@@ -491,10 +549,16 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
     VPL_CUDA(cudaFuncSetAttribute(k_gather<true>, cudaFuncAttributePreferredSharedMemoryCarveout, VPL_CARVEOUT));
 #endif
     if (d_ctr)
-        k_gather<true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue, clusters);
+        k_gather<true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue, clusters, chunk,
+                                            n_chunks, w.part, npix);
     else
-        k_gather<false><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue, clusters);
+        k_gather<false><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue, clusters, chunk,
+                                             n_chunks, w.part, npix);
     VPL_LAUNCHED("k_gather");
+    if (n_chunks > 1) {
+        k_gather_finish<<<nb(tm.n_warps() * 32, 128), 128, 0, s>>>(tm, d_gbuf, w.part, n_chunks, npix, d_rgb);
+        VPL_LAUNCHED("k_gather_finish");
+    }
     return VPL_OK;
 }
 

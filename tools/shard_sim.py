@@ -1,0 +1,80 @@
+"""Multi-GPU scaling estimate on one GPU: the G ranks of the
+pixel-tile sharding do not wait on one another (each gathers its own tiles
+with the replicated scene, BVH and VPLs), so each rank's gather can be timed
+alone, one after the other, on a single B200.  Reports, per G, every rank's
+gather time, the load-balance efficiency T(1) / (G * max_r T_r) of the
+gather, and the step efficiency once the replicated per-rank work (upload,
+BVH build, VPL generation, G-buffer of its tiles) and the collectives
+(broadcast of scene + VPLs, framebuffer reduce, at the measured 770 GB/s
+NVLink bus bandwidth of B200_PROFILING.md) are added.  This is an emulation:
+the driver's `bench.py --gpus N` runs are the measurement.
+
+  python tools/shard_sim.py --config 4 --gpus 2 4 8
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+import paper_2203_11484_b200 as V  # noqa: E402
+import scenegen  # noqa: E402
+from paper_2203_11484_b200.parallel import tiles_for_rank  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=4)
+ap.add_argument("--gpus", type=int, nargs="+", default=[2, 4, 8])
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+
+s = scenegen.make_scene(a.config)
+r = V.Renderer(s)
+torch.cuda.synchronize()
+ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+
+def timed(fn):
+    best = None
+    for _ in range(a.reps):
+        e0, e1 = ev(), ev()
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    return best
+
+
+# the replicated per-rank work of one step, timed once at full size (a1-a7 without the gather)
+def pre():
+    r.upload()
+    r.bvh, r._bwork = V.build_bvh(r.scene, r.n, r._bvh, r._bwork)
+    r._bvh = r.bvh
+    r.labels, r.n_near = V.classify_near_far(r.scene, r.n, s.T)
+    r.vpls, r.info, r._gwork = V.generate_vpls(r.scene, r.bvh, r.labels, r.n, s.M, s.K_near, s.max_depth, s.rr,
+                                               s.seed, max_out=r.max_out, vpls=r._vbuf, work=r._gwork)
+
+
+t_pre = timed(pre)
+t_gb = timed(lambda: V.render_gbuffer(r.scene, r.bvh, r.tiles, s.width, s.height, 16, 16, r.gbuf))
+t1 = timed(lambda: V.gather_indirect(r.scene, r.bvh, r.gbuf, r.vpls, r.tiles, s.width, s.height, 16, 16, r.rgb))
+bw = 770e9
+coll_ms = ((s.verts.nbytes + s.albedo.nbytes + r.vpls.numel()) / bw + (s.width * s.height * 12) / bw) * 1e3
+out = {"config": s.name, "t1_gather_ms": t1, "replicated_ms": t_pre, "gbuffer_full_ms": t_gb,
+       "collectives_ms_est": coll_ms, "runs": []}
+step1 = t_pre + t_gb + t1
+for G in a.gpus:
+    tr = []
+    for rank in range(G):
+        tiles = tiles_for_rank(s.width, s.height, 16, 16, rank, G, device="cuda")
+        tr.append(timed(lambda: V.gather_indirect(r.scene, r.bvh, r.gbuf, r.vpls, tiles, s.width, s.height, 16, 16,
+                                                  r.rgb)))
+    tmax = max(tr)
+    stepG = t_pre + t_gb / G + tmax + coll_ms
+    out["runs"].append({"G": G, "rank_gather_ms": tr, "gather_efficiency": t1 / (G * tmax),
+                        "step_ms_est": stepG, "step_efficiency_est": step1 / (G * stepG)})
+print(json.dumps(out), flush=True)
