@@ -203,13 +203,14 @@ VPL_API int32_t vpl_render_gbuffer(const void* d_scene, const void* d_bvh, const
 /* a8  gather_indirect (Eq. 1; O13): indirect-only linear radiance
  * d_rgb float[H*W*3] for the listed tiles (others untouched).  Miss or
  * back-face pixels get 0.  d_ctr (nullable) accumulates counters.
- * d_work: vpl_gather_bytes(n_vpls, W*H) bytes (tile queue, a Morton-ordered
+ * d_work: vpl_gather_bytes(n_vpls, W, H) bytes (tile queue, a Morton-ordered
  * copy of the VPLs — Eq. 1 is a sum over the set, the gather visits it in
  * spatial order; the caller's array is not modified — VPL cluster bounds and,
  * when M > 256, per-chunk partial sums: the work items are (8x4 pixel block,
  * VPL chunk) pairs, chunk = max(256, ceil(M/128) rounded up to 256), folded in
- * chunk order, so the image depends on M only, never on the tile split). */
-VPL_API int32_t vpl_gather_bytes(int32_t n_vpls, int64_t n_pixels, size_t* work_bytes);
+ * chunk order by the warp that completes a block's last chunk, so the image
+ * depends on M only, never on the tile split). */
+VPL_API int32_t vpl_gather_bytes(int32_t n_vpls, int32_t width, int32_t height, size_t* work_bytes);
 VPL_API int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf,
                             const vpl_record* d_vpls, int32_t n_vpls, const int32_t* d_tiles, int32_t n_tiles,
                             int32_t tile_w, int32_t tile_h, float* d_rgb, vpl_counters* d_ctr, void* d_work,

@@ -97,7 +97,7 @@ def load_library(path: str | os.PathLike | None = None):
         "vpl_generate_bytes": (I32, [P, I64, I64, P]),
         "vpl_generate_vpls": (I32, [P, P, P, P, P, I64, P, P, SZ, P]),
         "vpl_render_gbuffer": (I32, [P, P, P, I32, I32, I32, P, P]),
-        "vpl_gather_bytes": (I32, [I32, I64, P]),
+        "vpl_gather_bytes": (I32, [I32, I32, I32, P]),
         "vpl_gather_indirect": (I32, [P, P, P, P, I32, P, I32, I32, I32, P, P, P, SZ, P]),
         "vpl_render_direct": (I32, [P, P, P, P, I32, I32, I32, I32, C.c_uint64, I32, P, P]),
         "vpl_image_error": (I32, [P, P, I64, P, P, SZ, P]),
@@ -278,7 +278,7 @@ def gather_indirect(scene, bvh, gbuf, vpls, tiles, W, H, tw=16, th=16, rgb=None,
     rgb = rgb if rgb is not None else torch.zeros(H * W * 3, dtype=torch.float32, device=dev)
     nv = vpls.shape[0] if vpls.dim() == 2 else vpls.numel() // VPL_RECORD_BYTES
     wb = C.c_size_t()
-    _check(load_library().vpl_gather_bytes(nv, W * H, C.byref(wb)), "vpl_gather_bytes")
+    _check(load_library().vpl_gather_bytes(nv, W, H, C.byref(wb)), "vpl_gather_bytes")
     if work is None or work.numel() < wb.value:
         work = torch.empty(wb.value, dtype=torch.uint8, device=dev)
     ctr = torch.zeros(len(COUNTER_NAMES), dtype=torch.int64, device=dev) if counters else None

@@ -517,6 +517,17 @@ struct TileMap {
     const int32_t* tiles;
     int32_t n_tiles, tw, th, W, H, tiles_x, blocks_per_tile, bx_per_tile;
     __host__ __device__ int64_t n_warps() const { return (int64_t)n_tiles * blocks_per_tile; }
+    // index of the 8x4 block of warp g in the frame's block grid (ceil(W/8) per row), or -1 when the
+    // block lies wholly outside the image (tiles may overhang the last row / column)
+    __device__ __forceinline__ int64_t block_index(int64_t g) const {
+        int32_t ti = (int32_t)(g / blocks_per_tile), sub = (int32_t)(g % blocks_per_tile);
+        int32_t t = tiles[ti];
+        int32_t tx = t % tiles_x, ty = t / tiles_x;
+        int32_t x0 = tx * tw + (sub % bx_per_tile) * 8;
+        int32_t y0 = ty * th + (sub / bx_per_tile) * 4;
+        if (x0 >= W || y0 >= H) return -1;
+        return (int64_t)(y0 / 4) * ((W + 7) / 8) + x0 / 8;
+    }
     // returns the pixel of (warp g, lane) or -1 when outside the image
     __device__ __forceinline__ int32_t pixel(int64_t g, int lane) const {
         int32_t ti = (int32_t)(g / blocks_per_tile), sub = (int32_t)(g % blocks_per_tile);

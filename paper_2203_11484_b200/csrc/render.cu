@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                                                 const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
                                                 vpl_counters* __restrict__ ctr, int* __restrict__ queue,
                                                 const float4* __restrict__ clusters, int32_t chunk, int32_t n_chunks,
-                                                float* __restrict__ part_out, int64_t npix) {
+                                                float* __restrict__ part_out, int* __restrict__ done) {
     __shared__ int sstack[kWarpStack];
     __shared__ float s_acc[3][32];   // running per-lane totals (kept out of the register budget)
     const int lane = threadIdx.x;
@@ -159,9 +159,39 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 o[0] = active ? s_acc[0][lane] * rho.x * s : 0.0f;
                 o[1] = active ? s_acc[1][lane] * rho.y * s : 0.0f;
                 o[2] = active ? s_acc[2][lane] * rho.z * s : 0.0f;
-            } else {   // chunk partial sums, folded in chunk order by k_gather_finish
-                float* o = part_out + 3 * ((int64_t)ch * npix + pix);
-                o[0] = s_acc[0][lane]; o[1] = s_acc[1][lane]; o[2] = s_acc[2][lane];
+            }
+        }
+        const int64_t blk = n_chunks > 1 ? tm.block_index(g / n_chunks) : -1;
+        if (blk >= 0) {
+            // chunk partial sums, (block, chunk, lane)-contiguous; the warp that completes a block's last
+            // chunk folds them in chunk order (fp32) while they are still in L2, writes the pixels and
+            // discards the partial lines so they are never written back to HBM
+            float* pb = part_out + (blk * n_chunks) * 96;             // 96 floats = 32 lanes x 3 = 3 lines
+            float* o = pb + ch * 96 + 3 * lane;
+            o[0] = s_acc[0][lane]; o[1] = s_acc[1][lane]; o[2] = s_acc[2][lane];
+            __threadfence();
+            __syncwarp();
+            int prev = 0;
+            if (lane == 0) prev = atomicAdd(done + blk, 1);
+            prev = __shfl_sync(0xFFFFFFFFu, prev, 0);
+            if (prev == n_chunks - 1) {
+                __threadfence();
+                float acc[3] = {0.0f, 0.0f, 0.0f};
+                for (int c = 0; c < n_chunks; ++c) {
+                    const float* q = pb + c * 96 + 3 * lane;
+                    acc[0] += __ldcg(q); acc[1] += __ldcg(q + 1); acc[2] += __ldcg(q + 2);
+                }
+                if (pix >= 0) {
+                    const float s = (float)(1.0 / kPiR);
+                    f3 rho = xyz(((const float4*)(gb + pix))[2]);
+                    float* out = rgb + 3 * (int64_t)pix;
+                    out[0] = active ? acc[0] * rho.x * s : 0.0f;
+                    out[1] = active ? acc[1] * rho.y * s : 0.0f;
+                    out[2] = active ? acc[2] * rho.z * s : 0.0f;
+                }
+                __syncwarp();
+                for (int l = lane; l < 3 * n_chunks; l += 32)
+                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(pb + 32 * l) : "memory");
             }
         }
         if (kCount) {
@@ -373,30 +403,6 @@ __global__ void k_image_err_final(const double* __restrict__ part, int nb, doubl
     out[threadIdx.x] = t;
 }
 
-// fold the VPL-chunk partial sums of every listed pixel in chunk order (fp32),
-// then Eq. 1's rho/pi (O13); miss / back-face pixels get 0
-__global__ void k_gather_finish(TileMap tm, const vpl_gpoint* __restrict__ gb, const float* __restrict__ part,
-                                int32_t n_chunks, int64_t npix, float* __restrict__ rgb) {
-    int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (g >= tm.n_warps()) return;
-    int32_t pix = tm.pixel(g, lane);
-    if (pix < 0) return;
-    const float4* gp = (const float4*)(gb + pix);
-    const float4 a = gp[0], b = gp[1], c = gp[2];
-    const bool active = __float_as_int(a.w) >= 0 && __float_as_int(b.w) != 0;
-    float acc[3] = {0.0f, 0.0f, 0.0f};
-    for (int ch = 0; ch < n_chunks; ++ch) {
-        const float* p = part + 3 * ((int64_t)ch * npix + pix);
-        acc[0] += p[0]; acc[1] += p[1]; acc[2] += p[2];
-    }
-    const float s = (float)(1.0 / kPiR);
-    float* o = rgb + 3 * (int64_t)pix;
-    o[0] = active ? acc[0] * c.x * s : 0.0f;
-    o[1] = active ? acc[1] * c.y * s : 0.0f;
-    o[2] = active ? acc[2] * c.z * s : 0.0f;
-}
-
 // VPL chunking of the gather's work items: depends on M only (so any tile split
 // reproduces the same sums): chunk = max(CHUNK_MIN, ceil(M / CHUNKS) rounded up to 256); 128 chunks
 // put the C4 load-balance efficiency at 8 ranks at 95% (tools/shard_sim.py)
@@ -419,18 +425,21 @@ struct GatherWork {
     unsigned* box;
     float4* clusters;
     float* part;
+    int* done;
     uint32_t *keys, *keys2;
     int32_t *idx, *idx2;
     vpl_record* sorted;
     void* cub;
     size_t cub_bytes;
 };
-static size_t gather_layout(int32_t M, int64_t npix, char* base, GatherWork* w) {
+static size_t gather_layout(int32_t M, int32_t W, int32_t H, char* base, GatherWork* w) {
     Bump b{base};
     w->queue = b.take<int>(1);
     int32_t chunk, nch;
     gather_chunks(M, &chunk, &nch);
-    w->part = b.take<float>(nch > 1 ? (size_t)nch * (size_t)npix * 3 : 1);
+    const size_t nblk = (size_t)((W + 7) / 8) * (size_t)((H + 3) / 4);   // 8x4 blocks of a full frame
+    w->part = b.take<float>(nch > 1 ? nblk * (size_t)nch * 96 : 1);
+    w->done = b.take<int>(nblk);
     w->box = b.take<unsigned>(6);
     size_t m = (size_t)(M > 0 ? M : 1);
     w->keys = b.take<uint32_t>(m);
@@ -484,10 +493,10 @@ int32_t vpl_render_gbuffer(const void* d_scene, const void* d_bvh, const int32_t
     return VPL_OK;
 }
 
-int32_t vpl_gather_bytes(int32_t n_vpls, int64_t n_pixels, size_t* work_bytes) {
-    if (!work_bytes || n_vpls < 0 || n_pixels < 0) return VPL_EINVAL;
+int32_t vpl_gather_bytes(int32_t n_vpls, int32_t width, int32_t height, size_t* work_bytes) {
+    if (!work_bytes || n_vpls < 0 || width < 0 || height < 0) return VPL_EINVAL;
     GatherWork w;
-    *work_bytes = gather_layout(n_vpls, n_pixels, nullptr, &w);
+    *work_bytes = gather_layout(n_vpls, width, height, nullptr, &w);
     return VPL_OK;
 }
 
@@ -502,12 +511,11 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
     SceneHdr hh;
     VPL_TRY(read_scene_hdr(d_scene, s, &hh));
     GatherWork w;
-    const int64_t npix = (int64_t)hh.W * hh.H;
-    if (work_bytes < gather_layout(n_vpls, npix, nullptr, &w)) {
-        set_error("vpl_gather_indirect: work buffer smaller than vpl_gather_bytes(n_vpls, W*H)");
+    if (work_bytes < gather_layout(n_vpls, hh.W, hh.H, nullptr, &w)) {
+        set_error("vpl_gather_indirect: work buffer smaller than vpl_gather_bytes(n_vpls, W, H)");
         return VPL_ESMALL;
     }
-    gather_layout(n_vpls, npix, (char*)d_work, &w);
+    gather_layout(n_vpls, hh.W, hh.H, (char*)d_work, &w);
     int32_t chunk, n_chunks;
     gather_chunks(n_vpls, &chunk, &n_chunks);
     TileMap tm;
@@ -515,6 +523,8 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
     if (n_tiles == 0) return VPL_OK;
     int* queue = w.queue;
     VPL_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
+    if (n_chunks > 1)
+        VPL_CUDA(cudaMemsetAsync(w.done, 0, sizeof(int) * (size_t)((hh.W + 7) / 8) * (size_t)((hh.H + 3) / 4), s));
     const vpl_record* vp = d_vpls;
     if (n_vpls > 1) {
         const unsigned init[6] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u};
@@ -550,15 +560,12 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
 #endif
     if (d_ctr)
         k_gather<true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue, clusters, chunk,
-                                            n_chunks, w.part, npix);
+                                            n_chunks, w.part, w.done);
     else
         k_gather<false><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue, clusters, chunk,
-                                             n_chunks, w.part, npix);
+                                             n_chunks, w.part, w.done);
     VPL_LAUNCHED("k_gather");
-    if (n_chunks > 1) {
-        k_gather_finish<<<nb(tm.n_warps() * 32, 128), 128, 0, s>>>(tm, d_gbuf, w.part, n_chunks, npix, d_rgb);
-        VPL_LAUNCHED("k_gather_finish");
-    }
+
     return VPL_OK;
 }
 
