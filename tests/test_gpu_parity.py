@@ -237,3 +237,20 @@ def test_single_triangle_scene():
     assert_vpls_bitwise(V.decode_vpls(v), ov)
     r = _gather_case(gs, os_, np.arange(128, dtype=np.int32), v)
     assert r["rgb"].max() == 0.0                         # every VPL is on the receiver's own triangle (R14)
+
+
+def test_gather_chunked_items_are_tile_split_invariant(scenes, gpu):
+    """C2 (M = 4096 -> 16 VPL chunks folded in-kernel): the union of disjoint
+    tile subsets equals the full frame bitwise, and repeated launches agree
+    bitwise (the fold order is fixed, the queue order is not)."""
+    s = scenes[2]
+    v, _ = gpu[2].generate()
+    gb, tiles = gpu[2].gbuffer()
+    full, _ = V.gather_indirect(gpu[2].scene, gpu[2].bvh, gb, v, tiles, s.width, s.height)
+    again, _ = V.gather_indirect(gpu[2].scene, gpu[2].bvh, gb, v, tiles, s.width, s.height)
+    assert torch.equal(full, again)
+    parts = torch.zeros_like(full)
+    for r in range(4):
+        V.gather_indirect(gpu[2].scene, gpu[2].bvh, gb, v, tiles[r::4].contiguous(), s.width, s.height, rgb=parts)
+    assert torch.equal(full, parts)
+    assert float(full.abs().max()) > 0
