@@ -123,7 +123,7 @@ typedef struct {
     unsigned long long tri_tests;    /* exact Moller-Trumbore tests (ray x triangle) */
     unsigned long long warp_rays;    /* packets that needed a traversal (>= 1 unresolved lane) */
     unsigned long long warp_steps;   /* warp-level traversal iterations (node or leaf visits) */
-    unsigned long long cone_tests;   /* packet-cone x child box tests (16-wide nodes) */
+    unsigned long long cone_tests;   /* beam x child box tests of real (non-empty) children of 16-wide nodes */
     unsigned long long cone_packets; /* packets traversed with the cone test */
     unsigned long long ray_packets;  /* packets traversed with per-ray tests (loose cones) */
     unsigned long long cache_hits;   /* traced lanes resolved by the occluder cache */

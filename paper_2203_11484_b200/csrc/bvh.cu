@@ -282,6 +282,9 @@ __device__ __forceinline__ void ref_box(int r, const float4* __restrict__ nbox, 
 }
 
 // greedy: open the inner child of largest surface area until kWide children
+#ifndef VPL_WIDE_SMALL
+#define VPL_WIDE_SMALL 2   // absorb inner children of <= 2 triangles first (C4: -0.7%)
+#endif
 #ifndef VPL_WIDE_OPEN
 #define VPL_WIDE_OPEN 0   // 16-wide collapse opens the inner child of 0: largest area, 1: most triangles, 2: area x triangles
 #endif
@@ -304,6 +307,9 @@ __global__ void k_wide_expand(const int* __restrict__ F, int nF, const int2* __r
                 float a = half_area(nbox[2 * ref[k]], nbox[2 * ref[k] + 1]);
                 if (kW == kWide && VPL_WIDE_OPEN == 1) a = (float)cnt[ref[k]];
                 if (kW == kWide && VPL_WIDE_OPEN == 2) a *= (float)cnt[ref[k]];
+                // absorb small subtrees first: an inner child of <= VPL_WIDE_SMALL triangles is opened
+                // before any large one, so it never becomes a nearly empty wide node of its own
+                if (kW == kWide && VPL_WIDE_SMALL > 0 && cnt[ref[k]] <= VPL_WIDE_SMALL) a = 3.0e38f;
                 if (a > ba) { ba = a; best = k; }
             }
         if (best < 0) break;

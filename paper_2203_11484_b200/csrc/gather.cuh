@@ -210,7 +210,7 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
     while (sp > 0) {
         const int idx = sp - 1 - half;
         const int node = idx >= 0 ? sstack[idx] : -1;
-        if (kCount && lane == 0) { st->wsteps += 1; st->cones += sp >= 2 ? 2 * kWide : kWide; }
+        if (kCount && lane == 0) st->wsteps += 1;
         sp = max(sp - 2, 0);
         // no branch: an empty half-step loads the root's children (cached) and masks the result
         const int nsafe = node >= 0 ? node : 0;
@@ -219,6 +219,10 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
         int ref = node >= 0 ? __float_as_int(lo.w) : INT_MIN;
         const int axis = __float_as_int(hi.w);
         const bool hit = (ref != INT_MIN) & beam_box(B, lo, hi);
+        if (kCount) {   // beam tests of real children only (empty slots are not algorithmic work)
+            const unsigned real = __ballot_sync(0xFFFFFFFFu, ref != INT_MIN);
+            if (lane == 0) st->cones += __popc(real);
+        }
         const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
         unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
         if (Bi) {
