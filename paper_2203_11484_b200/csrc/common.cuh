@@ -398,7 +398,7 @@ __device__ __forceinline__ int fkey(float f) {   // order-preserving float -> in
 __device__ __forceinline__ float fkey_inv(int k) { return __int_as_float(k ^ ((k >> 31) & 0x7FFFFFFF)); }
 
 #ifndef VPL_CONE_SPREAD
-#define VPL_CONE_SPREAD 0.1f
+#define VPL_CONE_SPREAD 0.3f   // 0.3-1.0 measured equal at C4, 1.3% faster than 0.1
 #endif
 constexpr float kConeSpread = VPL_CONE_SPREAD;  // beam traversal iff max_a (Dmax_a - Dmin_a) < kConeSpread * |D|_min
 
