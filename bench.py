@@ -176,6 +176,9 @@ def run_ours(args):
 
     def step(counters=False):
         if world > 1:
+            # the frame is assembled by an in-place SUM reduce into rank 0's buffer, so its
+            # other ranks' tiles must start from zero every step
+            r.rgb.zero_()
             dist.broadcast(d_verts, 0)
             dist.broadcast(d_alb, 0)
         r.upload(d_verts, d_alb, stream)

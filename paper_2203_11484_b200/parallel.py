@@ -45,7 +45,8 @@ def tile_pixel_mask(W, H, tw, th, tiles):
 def assemble(rgb_local: torch.Tensor, group=None, dst=0):
     """Framebuffer assembly: every rank holds a zero-initialised full frame
     with only its own tiles written; a SUM reduce to `dst` is bitwise equal to
-    gathering the tiles (x + 0 = x exactly)."""
+    gathering the tiles (x + 0 = x exactly).  The reduce is in place: `dst`'s
+    buffer then holds every rank's tiles, so zero it before the next frame."""
     import torch.distributed as dist
     dist.reduce(rgb_local, dst, op=dist.ReduceOp.SUM, group=group)
     return rgb_local
