@@ -28,10 +28,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--gpus", type=int, nargs="+", default=[2, 4, 8])
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--tile", type=int, nargs=2, default=[16, 16], help="partition tile w h (multiples of 8, 4)")
 a = ap.parse_args()
 
 s = scenegen.make_scene(a.config)
-r = V.Renderer(s)
+tw, th = a.tile
+r = V.Renderer(s, tw=tw, th=th)
 torch.cuda.synchronize()
 ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
@@ -60,18 +62,18 @@ def pre():
 
 
 t_pre = timed(pre)
-t_gb = timed(lambda: V.render_gbuffer(r.scene, r.bvh, r.tiles, s.width, s.height, 16, 16, r.gbuf))
-t1 = timed(lambda: V.gather_indirect(r.scene, r.bvh, r.gbuf, r.vpls, r.tiles, s.width, s.height, 16, 16, r.rgb))
+t_gb = timed(lambda: V.render_gbuffer(r.scene, r.bvh, r.tiles, s.width, s.height, tw, th, r.gbuf))
+t1 = timed(lambda: V.gather_indirect(r.scene, r.bvh, r.gbuf, r.vpls, r.tiles, s.width, s.height, tw, th, r.rgb))
 bw = 770e9
 coll_ms = ((s.verts.nbytes + s.albedo.nbytes + r.vpls.numel()) / bw + (s.width * s.height * 12) / bw) * 1e3
-out = {"config": s.name, "t1_gather_ms": t1, "replicated_ms": t_pre, "gbuffer_full_ms": t_gb,
+out = {"config": s.name, "tile": [tw, th], "t1_gather_ms": t1, "replicated_ms": t_pre, "gbuffer_full_ms": t_gb,
        "collectives_ms_est": coll_ms, "runs": []}
 step1 = t_pre + t_gb + t1
 for G in a.gpus:
     tr = []
     for rank in range(G):
-        tiles = tiles_for_rank(s.width, s.height, 16, 16, rank, G, device="cuda")
-        tr.append(timed(lambda: V.gather_indirect(r.scene, r.bvh, r.gbuf, r.vpls, tiles, s.width, s.height, 16, 16,
+        tiles = tiles_for_rank(s.width, s.height, tw, th, rank, G, device="cuda")
+        tr.append(timed(lambda: V.gather_indirect(r.scene, r.bvh, r.gbuf, r.vpls, tiles, s.width, s.height, tw, th,
                                                   r.rgb)))
     tmax = max(tr)
     stepG = t_pre + t_gb / G + tmax + coll_ms
