@@ -254,3 +254,26 @@ def test_gather_chunked_items_are_tile_split_invariant(scenes, gpu):
         V.gather_indirect(gpu[2].scene, gpu[2].bvh, gb, v, tiles[r::4].contiguous(), s.width, s.height, rgb=parts)
     assert torch.equal(full, parts)
     assert float(full.abs().max()) > 0
+
+
+@pytest.mark.parametrize("M", [257, 511, 1000])
+def test_gather_chunk_boundaries_against_oracle(M, scenes, orc):
+    """VPL counts just above a chunk multiple (2 chunks of 256 + 1, ...):
+    every chunk partial is folded, the image matches the oracle (C1, all
+    pixels) and the tile-split invariance holds."""
+    s0 = scenes[1]
+    s = scenegen.custom_scene(s0.verts, s0.albedo, s0.lights, s0.cam, s0.width, s0.height, M=M,
+                              K_near=int(0.75 * M + 0.5), max_depth=3, rr=1, seed=7, T=1.75)
+    gs = GpuScene(s)
+    v, info = gs.generate()
+    assert v.shape[0] == M
+    px = np.arange(s.width * s.height, dtype=np.int32)
+    r = _gather_case(gs, orc[1], px, v)
+    assert r["tmis"] == 0 and r["vmis"] <= max(1, VIS_TOL * r["ntr"])
+    assert r["mre"] <= MRE_TOL and r["prel"] <= PIXEL_TOL, {k: r[k] for k in ("mre", "prel")}
+    gb, tiles = gs.gbuffer()
+    full, _ = V.gather_indirect(gs.scene, gs.bvh, gb, v, tiles, s.width, s.height)
+    parts = torch.zeros_like(full)
+    for k in range(3):
+        V.gather_indirect(gs.scene, gs.bvh, gb, v, tiles[k::3].contiguous(), s.width, s.height, rgb=parts)
+    assert torch.equal(full, parts)
