@@ -33,6 +33,9 @@ namespace vplgi {
 #ifndef VPL_GROUP
 #define VPL_GROUP 1
 #endif
+#ifndef VPL_SMEM_ADDR
+#define VPL_SMEM_ADDR 1     // traversal stack accessed through a 32-bit shared-window address held in a register
+#endif
 #ifndef VPL_NO_ORDER
 #define VPL_NO_ORDER 0      // 1: push hit children in lane order (no near-to-far ordering)
 #endif
@@ -206,10 +209,18 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
     if (lane == 0) sstack[0] = bv.root;
     __syncwarp();
     int sp = 1;
+#if VPL_SMEM_ADDR
+    const unsigned sbase = (unsigned)__cvta_generic_to_shared(sstack);   // 32-bit shared-window address
+#endif
     // each step pops the top two (lanes 0-15 take the top one)
     while (sp > 0) {
         const int idx = sp - 1 - half;
+#if VPL_SMEM_ADDR
+        int node = -1;
+        if (idx >= 0) asm volatile("ld.shared.s32 %0, [%1];" : "=r"(node) : "r"(sbase + 4u * (unsigned)idx));
+#else
         const int node = idx >= 0 ? sstack[idx] : -1;
+#endif
         if (kCount && lane == 0) st->wsteps += 1;
         sp = max(sp - 2, 0);
         // no branch: an empty half-step loads the root's children (cached) and masks the result
@@ -235,7 +246,12 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
             const bool rev = (dir_neg >> axis) & 1u;   // segments run x -> y along -axis: visit descending
             const int pos = (half ? 0 : nB) + (rev ? rank : nh - 1 - rank);   // first to visit ends on top
 #endif
+#if VPL_SMEM_ADDR
+            if (hit && ref >= 0)
+                asm volatile("st.shared.s32 [%0], %1;" ::"r"(sbase + 4u * (unsigned)(sp + pos)), "r"(ref) : "memory");
+#else
             if (hit && ref >= 0) sstack[sp + pos] = ref;
+#endif
             sp += nA + nB;
         }
         __syncwarp();
