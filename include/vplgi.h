@@ -42,7 +42,7 @@ extern "C" {
 #define VPL_API
 #endif
 
-#define VPL_ABI_VERSION 1
+#define VPL_ABI_VERSION 2   /* 2: vpl_gather_bytes(M, W, H), vpl_counters.cache_tests, f1-f4 entry points */
 #define VPL_MAX_LIGHTS 64
 
 enum {
