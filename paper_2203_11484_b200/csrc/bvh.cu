@@ -192,6 +192,92 @@ __global__ void k_sah_collapse(int64_t n, const int2* __restrict__ child, const 
     }
 }
 
+// 16-wide collapse by dynamic programming (VPL_WIDE_DP).  The beam traversal
+// pays one half-step per visited 16-wide node whatever its fill, and every
+// triangle is its own child slot, so the expected traversal cost is
+// sum over wide nodes w of A(w) (surface area ~ visit probability) plus a term
+// that does not depend on the collapse.  Bottom up over the binary tree:
+//   g(n, i) = least cost of covering n's subtree with <= i child slots,
+//             a slot being a triangle (cost 0) or a wide node m (cost f(m));
+//   f(n)    = A(n) + min_j g(L, j) + g(R, 16 - j)     (n as a wide node);
+//   g(n, 1) = f(n) (inner) or 0 (leaf);  g(n, i) = min(g(n, i-1), min_j g(L, j) + g(R, i - j)).
+// choice[n][i] = 0 when g(n, i) = g(n, i - 1), else the split j; choice[n][0] = the split of f(n).
+__global__ void k_wide_dp(int64_t n, const int2* __restrict__ child, const float4* __restrict__ nbox,
+                          const int* __restrict__ parent_int, const int* __restrict__ parent_leaf,
+                          int* __restrict__ flags, float* __restrict__ g, uint8_t* __restrict__ choice) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int node = parent_leaf[p];
+    while (node >= 0) {
+        __threadfence();
+        if (atomicAdd(&flags[node], 1) == 0) return;
+        __threadfence();
+        const int2 c = child[node];
+        float gl[kWide + 1], gr[kWide + 1];
+#pragma unroll
+        for (int i = 1; i <= kWide; ++i) {
+            gl[i] = c.x >= 0 ? __ldcg(g + (int64_t)c.x * kWide + (i - 1)) : 0.0f;
+            gr[i] = c.y >= 0 ? __ldcg(g + (int64_t)c.y * kWide + (i - 1)) : 0.0f;
+        }
+        uint8_t ch[kWide + 1];
+        float best16 = 3.0e38f;
+        int j16 = 1;
+        for (int j = 1; j < kWide; ++j) {
+            const float v = gl[j] + gr[kWide - j];
+            if (v < best16) { best16 = v; j16 = j; }
+        }
+        const float f = half_area(nbox[2 * node], nbox[2 * node + 1]) + best16;
+        ch[0] = (uint8_t)j16;
+        float prev = f;
+        __stcg(g + (int64_t)node * kWide + 0, f);
+        ch[1] = 0;
+        for (int i = 2; i <= kWide; ++i) {
+            float bi = 3.0e38f;
+            int ji = 1;
+            for (int j = 1; j < i; ++j) {
+                const float v = gl[j] + gr[i - j];
+                if (v < bi) { bi = v; ji = j; }
+            }
+            if (prev <= bi) { ch[i] = 0; } else { ch[i] = (uint8_t)ji; prev = bi; }
+            __stcg(g + (int64_t)node * kWide + (i - 1), prev);
+        }
+        for (int i = 0; i <= kWide; ++i) choice[(int64_t)node * (kWide + 1) + i] = ch[i];
+        node = parent_int[node];
+    }
+}
+
+// slots of wide node b from the DP choices: (node, i) pairs on a small stack
+__global__ void k_wide_expand_dp(const int* __restrict__ F, int nF, const int2* __restrict__ child,
+                                 const uint8_t* __restrict__ choice, int* __restrict__ exp, int* __restrict__ nint) {
+    int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nF) return;
+    const int b = F[f];
+    int st_n[2 * kWide], st_i[2 * kWide];
+    int sp = 0, cntc = 0, ni = 0;
+    const int2 cb = child[b];
+    const int j0 = choice[(int64_t)b * (kWide + 1) + 0];
+    st_n[sp] = cb.y; st_i[sp++] = kWide - j0;
+    st_n[sp] = cb.x; st_i[sp++] = j0;
+    while (sp > 0) {
+        const int nd = st_n[--sp];
+        int i = st_i[sp];
+        if (nd < 0 || i == 1) {             // a triangle, or an inner node that becomes a wide node
+            exp[f * kWide + cntc++] = nd;
+            ni += nd >= 0;
+            continue;
+        }
+        const uint8_t* cn = choice + (int64_t)nd * (kWide + 1);
+        while (i > 1 && cn[i] == 0) --i;    // fewer slots cover it at the same cost
+        if (i == 1) { exp[f * kWide + cntc++] = nd; ++ni; continue; }
+        const int j = cn[i];
+        const int2 cc = child[nd];
+        st_n[sp] = cc.y; st_i[sp++] = i - j;
+        st_n[sp] = cc.x; st_i[sp++] = j;
+    }
+    for (int k = cntc; k < kWide; ++k) exp[f * kWide + k] = INT_MIN;
+    nint[f] = ni;
+}
+
 // depth-first triangle offset of every node (leaves: index ~p -> slot n-1+p)
 __global__ void k_dfs_offsets(int64_t n, const int2* __restrict__ child, const int* __restrict__ parent_int,
                               const int* __restrict__ parent_leaf, const int* __restrict__ cnt, int* __restrict__ off,
@@ -282,6 +368,9 @@ __device__ __forceinline__ void ref_box(int r, const float4* __restrict__ nbox, 
 }
 
 // greedy: open the inner child of largest surface area until kWide children
+#ifndef VPL_WIDE_DP
+#define VPL_WIDE_DP 0     // 1: the 16-wide collapse by dynamic programming (least total wide-node area)
+#endif
 #ifndef VPL_WIDE_SMALL
 #define VPL_WIDE_SMALL 2   // absorb inner children of <= 2 triangles first (C4: -0.7%)
 #endif
@@ -473,6 +562,8 @@ struct BuildWork {
     int *nn, *parent_int, *parent_leaf, *flags, *cnt, *off, *totals, *icount, *pre;
     uint8_t* hidden;
     int *F0, *F1, *wexp, *nint, *noff;
+    float* dpg;
+    uint8_t* dpc;
     unsigned long long *mflags, *moff;
     float* cost;
     uint8_t* collapsed;
@@ -508,6 +599,8 @@ static size_t build_layout(int64_t n, char* base, BuildWork* w) {
     w->F0 = b.take<int>(n);
     w->F1 = b.take<int>(n);
     w->wexp = b.take<int>((size_t)kWide * n);
+    w->dpg = b.take<float>(VPL_WIDE_DP ? (size_t)kWide * n : 1);
+    w->dpc = b.take<uint8_t>(VPL_WIDE_DP ? (size_t)(kWide + 1) * n : 1);
     w->nint = b.take<int>(n);
     w->noff = b.take<int>(n);
     w->child = b.take<int2>(n);
@@ -594,6 +687,11 @@ int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* 
         k_sah_collapse<<<nblk(n, 256), 256, 0, s>>>(n, w.child, w.nbox, w.lbox, w.parent_int, w.parent_leaf, w.flags,
                                                     w.cnt, w.cost, w.collapsed, w.icount);
         VPL_LAUNCHED("k_sah_collapse");
+#if VPL_WIDE_DP
+        VPL_CUDA(cudaMemsetAsync(w.flags, 0, sizeof(int) * n, s));
+        k_wide_dp<<<nblk(n, 128), 128, 0, s>>>(n, w.child, w.nbox, w.parent_int, w.parent_leaf, w.flags, w.dpg, w.dpc);
+        VPL_LAUNCHED("k_wide_dp");
+#endif
         VPL_CUDA(cudaMemsetAsync(w.totals + 2, 0, sizeof(int), s));
         k_dfs_offsets<<<nblk(2 * n - 1, 256), 256, 0, s>>>(n, w.child, w.parent_int, w.parent_leaf, w.cnt, w.off,
                                                            w.totals + 2, w.icount, w.collapsed, w.pre, w.hidden);
@@ -610,7 +708,9 @@ int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* 
             int *Fc = w.F0, *Fn = w.F1;
             while (nF > 0) {
                 ++levels;
-                if (fmt == 0) k_wide_expand<kWide><<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.child, w.nbox, w.collapsed,
+                if (fmt == 0 && VPL_WIDE_DP)
+                    k_wide_expand_dp<<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.child, w.dpc, w.wexp, w.nint);
+                else if (fmt == 0) k_wide_expand<kWide><<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.child, w.nbox, w.collapsed,
                                                                               w.cnt, w.wexp, w.nint);
                 else k_wide_expand<kWide4><<<nblk(nF, 128), 128, 0, s>>>(Fc, nF, w.child, w.nbox, w.collapsed,
                                                                          w.cnt, w.wexp, w.nint);
