@@ -40,7 +40,7 @@ def _check_gather(r, o, px):
     return dict(tmis=tmis, vmis=vmis, ntr=ntr, mre=mre, prel=prel, agree=float(agree.mean()))
 
 
-@pytest.mark.parametrize("cfg,n_px", [(3, 64), (4, 16)])
+@pytest.mark.parametrize("cfg,n_px", [(3, 256), (4, 36)])
 def test_full_frame_parity(cfg, n_px):
     s = scenegen.make_scene(cfg)
     r = _frame(s)
