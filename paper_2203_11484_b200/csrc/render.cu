@@ -29,7 +29,10 @@ __global__ void k_gbuffer(SceneView sv, BvhView bv, TileMap tm, vpl_gpoint* __re
 // ci = n_i.(x - y) > 0 are both possible over the boxes; the bounds are
 // evaluated with a relative margin far above the fp32 rounding of O13's cull,
 // so a skipped cluster holds no traced pair (the image is unchanged bitwise).
-constexpr int kCluster = 32;
+#ifndef VPL_CLUSTER
+#define VPL_CLUSTER 32
+#endif
+constexpr int kCluster = VPL_CLUSTER;   // VPLs per culling cluster (divides 256)
 __device__ __forceinline__ bool cluster_may_trace(const float4* __restrict__ cb, f3 x, f3 nx) {
     const float4 ylo = __ldg(cb), yhi = __ldg(cb + 1), nlo = __ldg(cb + 2), nhi = __ldg(cb + 3);
     // max over y in the box of n_x.(y - x): per axis the larger of n*(lo - x), n*(hi - x)
@@ -49,26 +52,21 @@ __device__ __forceinline__ bool cluster_may_trace(const float4* __restrict__ cb,
     return (ax + ay) + az > -m && (bx + by) + bz > -m;
 }
 __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, float4* __restrict__ cb) {
-    const int c = blockIdx.x, lane = threadIdx.x;
-    const int i = c * kCluster + lane;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;     // one thread per cluster
+    if ((int64_t)c * kCluster >= M) return;
     const float inf = __int_as_float(0x7f800000);
     float4 a = make_float4(inf, inf, inf, 0.0f), b = make_float4(-inf, -inf, -inf, 0.0f);
     float4 na = a, nb = b;
-    if (i < M) {
+    const int i1 = min(M, (c + 1) * kCluster);
+    for (int i = c * kCluster; i < i1; ++i) {
         const float4* p = (const float4*)(v + i);
         const float4 y = p[0], n = p[1];
-        a = make_float4(y.x, y.y, y.z, 0.0f); b = a;
-        na = make_float4(n.x, n.y, n.z, 0.0f); nb = na;
+        a.x = fminf(a.x, y.x); a.y = fminf(a.y, y.y); a.z = fminf(a.z, y.z);
+        b.x = fmaxf(b.x, y.x); b.y = fmaxf(b.y, y.y); b.z = fmaxf(b.z, y.z);
+        na.x = fminf(na.x, n.x); na.y = fminf(na.y, n.y); na.z = fminf(na.z, n.z);
+        nb.x = fmaxf(nb.x, n.x); nb.y = fmaxf(nb.y, n.y); nb.z = fmaxf(nb.z, n.z);
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        a.x = fminf(a.x, __shfl_xor_sync(0xFFFFFFFFu, a.x, o)); b.x = fmaxf(b.x, __shfl_xor_sync(0xFFFFFFFFu, b.x, o));
-        a.y = fminf(a.y, __shfl_xor_sync(0xFFFFFFFFu, a.y, o)); b.y = fmaxf(b.y, __shfl_xor_sync(0xFFFFFFFFu, b.y, o));
-        a.z = fminf(a.z, __shfl_xor_sync(0xFFFFFFFFu, a.z, o)); b.z = fmaxf(b.z, __shfl_xor_sync(0xFFFFFFFFu, b.z, o));
-        na.x = fminf(na.x, __shfl_xor_sync(0xFFFFFFFFu, na.x, o)); nb.x = fmaxf(nb.x, __shfl_xor_sync(0xFFFFFFFFu, nb.x, o));
-        na.y = fminf(na.y, __shfl_xor_sync(0xFFFFFFFFu, na.y, o)); nb.y = fmaxf(nb.y, __shfl_xor_sync(0xFFFFFFFFu, nb.y, o));
-        na.z = fminf(na.z, __shfl_xor_sync(0xFFFFFFFFu, na.z, o)); nb.z = fmaxf(nb.z, __shfl_xor_sync(0xFFFFFFFFu, nb.z, o));
-    }
-    if (lane == 0) { cb[4 * c] = a; cb[4 * c + 1] = b; cb[4 * c + 2] = na; cb[4 * c + 3] = nb; }
+    cb[4 * c] = a; cb[4 * c + 1] = b; cb[4 * c + 2] = na; cb[4 * c + 3] = nb;
 }
 
 // One warp per CTA: the traversal stack is then at a fixed shared-memory
@@ -123,7 +121,7 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             for (int i0 = vbeg; i0 < vend; i0 += 256) {
                 float part[3] = {0.0f, 0.0f, 0.0f};
                 const int i1 = min(vend, i0 + 256);
-                for (int c0 = i0; c0 < i1; c0 += kCluster) {       // clusters of 32 VPLs (i0 % 32 == 0)
+                for (int c0 = i0; c0 < i1; c0 += kCluster) {       // clusters of kCluster VPLs (i0 % 256 == 0)
                     if (clusters &&
                         !__any_sync(0xFFFFFFFFu, active && cluster_may_trace(clusters + 4 * (c0 / kCluster), x, nx)))
                         continue;                                      // no lane can trace any VPL of it
@@ -447,7 +445,7 @@ static size_t gather_layout(int32_t M, int32_t W, int32_t H, char* base, GatherW
     w->idx = b.take<int32_t>(m);
     w->idx2 = b.take<int32_t>(m);
     w->sorted = b.take<vpl_record>(m);
-    w->clusters = b.take<float4>(4 * ((m + 31) / 32));
+    w->clusters = b.take<float4>(4 * ((m + kCluster - 1) / kCluster));
     size_t c = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, c, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
                                     (int32_t*)nullptr, (int)m, 0, 30);
@@ -542,7 +540,8 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
     const float4* clusters = nullptr;
 #if VPL_CLUSTER_CULL
     if (n_vpls > 0) {
-        k_vpl_clusters<<<(n_vpls + kCluster - 1) / kCluster, kCluster, 0, s>>>(vp, n_vpls, w.clusters);
+        const int ncl = (n_vpls + kCluster - 1) / kCluster;
+        k_vpl_clusters<<<nb(ncl, 128), 128, 0, s>>>(vp, n_vpls, w.clusters);
         VPL_LAUNCHED("k_vpl_clusters");
         clusters = w.clusters;
     }
