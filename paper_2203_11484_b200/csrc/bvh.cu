@@ -20,6 +20,7 @@ namespace vplgi {
 #endif
 constexpr int kPlocRadius = VPL_PLOC_RADIUS;
 constexpr int kPlocBlock = 256;
+constexpr int kPlocBatch = 4;   // PLOC iterations per host round trip
 constexpr int kMaxLeaf = 4;
 constexpr float kCostTri = 1.0f;   // one exact MT test  (~35 thread-ops)
 constexpr float kCostNode = 1.0f;  // one node visit = two slab tests (~34 thread-ops)
@@ -84,9 +85,17 @@ __device__ __forceinline__ float merged_area(float4 alo, float4 ahi, float4 blo,
 }
 
 // nearest neighbour within +-r in Morton order by merged surface area (ties -> lower index)
-__global__ void __launch_bounds__(kPlocBlock) k_ploc_nn(const float4* __restrict__ cl, int C, int* __restrict__ nn) {
+// PLOC iterations run in batches without a host round trip: the cluster count
+// C and the next free node id live in device memory (double-buffered by
+// iteration parity), grids are sized by the last count the host saw (C only
+// shrinks), and threads beyond the current C do nothing (flags write 0, so
+// the scan over the host bound is exact).
+__global__ void __launch_bounds__(kPlocBlock) k_ploc_nn(const float4* __restrict__ cl, const int* __restrict__ dC,
+                                                        int* __restrict__ nn) {
     __shared__ float4 slo[kPlocBlock + 2 * kPlocRadius], shi[kPlocBlock + 2 * kPlocRadius];
+    const int C = *dC;
     int b0 = blockIdx.x * kPlocBlock;
+    if (b0 >= C) return;
     for (int k = threadIdx.x; k < kPlocBlock + 2 * kPlocRadius; k += blockDim.x) {
         int j = b0 - kPlocRadius + k;
         if (j >= 0 && j < C) { slo[k] = cl[2 * j]; shi[k] = cl[2 * j + 1]; }
@@ -109,9 +118,12 @@ __global__ void __launch_bounds__(kPlocBlock) k_ploc_nn(const float4* __restrict
 }
 
 // flags: bit 32.. = merge (this cluster absorbs nn[i]), bit 0 = keep
-__global__ void k_ploc_flags(const int* __restrict__ nn, int C, unsigned long long* __restrict__ flags) {
+__global__ void k_ploc_flags(const int* __restrict__ nn, const int* __restrict__ dC, int Cub,
+                             unsigned long long* __restrict__ flags) {
+    const int C = *dC;
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= C) return;
+    if (i >= Cub) return;
+    if (i >= C) { flags[i] = 0ull; return; }
     int j = nn[i];
     bool mutual = j >= 0 && nn[j] == i;
     unsigned long long merge = (mutual && i < j) ? 1ull : 0ull;
@@ -119,16 +131,22 @@ __global__ void k_ploc_flags(const int* __restrict__ nn, int C, unsigned long lo
     flags[i] = (merge << 32) | keep;
 }
 
-__global__ void k_ploc_merge(const float4* __restrict__ cl, const int* __restrict__ nn, int C,
+__global__ void k_ploc_merge(const float4* __restrict__ cl, const int* __restrict__ nn, const int* __restrict__ dC,
                              const unsigned long long* __restrict__ flags, const unsigned long long* __restrict__ off,
-                             int next_id, float4* __restrict__ out, int2* __restrict__ child, float4* __restrict__ nbox,
-                             int* __restrict__ parent_int, int* __restrict__ parent_leaf, int* __restrict__ totals) {
+                             const int* __restrict__ dNext, float4* __restrict__ out, int2* __restrict__ child,
+                             float4* __restrict__ nbox, int* __restrict__ parent_int, int* __restrict__ parent_leaf,
+                             int* __restrict__ dCout, int* __restrict__ dNextOut, int* __restrict__ totals) {
+    const int C = *dC, next_id = *dNext;
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= C) return;
     unsigned long long f = flags[i], o = off[i];
     int keep = (int)(f & 1ull), merge = (int)(f >> 32);
     int ko = (int)(o & 0xFFFFFFFFull), mo = (int)(o >> 32);
-    if (i == C - 1) { totals[0] = ko + keep; totals[1] = mo + merge; }
+    if (i == C - 1) {
+        totals[0] = ko + keep; totals[1] = mo + merge;
+        *dCout = ko + keep;
+        *dNextOut = next_id - (mo + merge);
+    }
     if (!keep) return;
     float4 alo = cl[2 * i], ahi = cl[2 * i + 1];
     if (!merge) {
@@ -588,7 +606,7 @@ static size_t build_layout(int64_t n, char* base, BuildWork* w) {
     w->flags = b.take<int>(n);
     w->cnt = b.take<int>(n);
     w->off = b.take<int>(2 * n);
-    w->totals = b.take<int>(4);
+    w->totals = b.take<int>(8);
     w->mflags = b.take<unsigned long long>(n);
     w->moff = b.take<unsigned long long>(n);
     w->cost = b.take<float>(n);
@@ -660,28 +678,40 @@ int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* 
     VPL_LAUNCHED("k_leaf_clusters");
 
     if (n > 1) {
-        // PLOC: merge mutual nearest neighbours until one cluster is left
-        int C = (int)n, next_id = (int)n - 2;
+        // PLOC: merge mutual nearest neighbours until one cluster is left, kPlocBatch
+        // iterations per host round trip (counts double-buffered in w.totals[4..7])
+        int C = (int)n;
         float4 *cur = w.clA, *nxt = w.clB;
         VPL_CUDA(cudaMemsetAsync(w.parent_int, 0xFF, sizeof(int) * n, s));
-        int tot[2];
+        int init[4] = {(int)n, (int)n, (int)n - 2, (int)n - 2};   // C[0], C[1], next[0], next[1]
+        VPL_CUDA(cudaMemcpyAsync(w.totals + 4, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        int* dC = w.totals + 4;      // dC[it & 1] = clusters entering iteration it
+        int* dN = w.totals + 6;      // dN[it & 1] = next free node id entering iteration it
+        int it = 0;
         while (C > 1) {
-            k_ploc_nn<<<nblk(C, kPlocBlock), kPlocBlock, 0, s>>>(cur, C, w.nn);
-            VPL_LAUNCHED("k_ploc_nn");
-            k_ploc_flags<<<nblk(C, 256), 256, 0, s>>>(w.nn, C, w.mflags);
-            VPL_LAUNCHED("k_ploc_flags");
-            cb = w.cub_bytes;
-            VPL_CUDA(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.mflags, w.moff, C, s));
-            k_ploc_merge<<<nblk(C, 256), 256, 0, s>>>(cur, w.nn, C, w.mflags, w.moff, next_id, nxt, w.child, w.nbox,
-                                                      w.parent_int, w.parent_leaf, w.totals);
-            VPL_LAUNCHED("k_ploc_merge");
-            VPL_CUDA(cudaMemcpyAsync(tot, w.totals, sizeof(tot), cudaMemcpyDeviceToHost, s));
+            const int Cub = C;
+            for (int b = 0; b < kPlocBatch; ++b, ++it) {
+                const int pi = it & 1, po = pi ^ 1;
+                k_ploc_nn<<<nblk(Cub, kPlocBlock), kPlocBlock, 0, s>>>(cur, dC + pi, w.nn);
+                VPL_LAUNCHED("k_ploc_nn");
+                k_ploc_flags<<<nblk(Cub, 256), 256, 0, s>>>(w.nn, dC + pi, Cub, w.mflags);
+                VPL_LAUNCHED("k_ploc_flags");
+                cb = w.cub_bytes;
+                VPL_CUDA(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.mflags, w.moff, Cub, s));
+                k_ploc_merge<<<nblk(Cub, 256), 256, 0, s>>>(cur, w.nn, dC + pi, w.mflags, w.moff, dN + pi, nxt, w.child,
+                                                            w.nbox, w.parent_int, w.parent_leaf, dC + po, dN + po,
+                                                            w.totals);
+                VPL_LAUNCHED("k_ploc_merge");
+                float4* t = cur; cur = nxt; nxt = t;
+            }
+            int cnow = 0;
+            VPL_CUDA(cudaMemcpyAsync(&cnow, dC + (it & 1), sizeof(int), cudaMemcpyDeviceToHost, s));
             VPL_CUDA(cudaStreamSynchronize(s));
-            if (tot[1] <= 0) { set_error("vpl_build_bvh: PLOC made no progress"); return VPL_ECUDA; }
-            C = tot[0];
-            next_id -= tot[1];
-            float4* t = cur; cur = nxt; nxt = t;
+            if (cnow >= C && C > 1) { set_error("vpl_build_bvh: PLOC made no progress"); return VPL_ECUDA; }
+            C = cnow;
         }
+        // a finished batch may have run idle iterations (C = 1): they copy the root
+        // cluster between the ping-pong buffers and change nothing else
         // SAH collapse, depth-first ordering, emission
         VPL_CUDA(cudaMemsetAsync(w.flags, 0, sizeof(int) * n, s));
         k_sah_collapse<<<nblk(n, 256), 256, 0, s>>>(n, w.child, w.nbox, w.lbox, w.parent_int, w.parent_leaf, w.flags,
