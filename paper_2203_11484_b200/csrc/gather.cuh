@@ -1,27 +1,25 @@
 // gather.cuh — the warp-cooperative shadow-ray engine of the a8 gather
 // (Eq. 1; DESIGN.md §3 O13 and §5).
 //
-// A warp owns 32 receivers x_j (one per lane).  It walks the VPL array in
-// order, in *groups* of up to kGroup consecutive VPLs whose positions lie
-// close together (consecutive near VPLs are neighbouring strata of the
-// Morton-ordered patch table).  For a group, every lane computes the
-// Eq. 1 cosine terms of its receiver against each VPL of the group (exact
-// fp32, O13), and the shadow segments x_j -> y_k that need a visibility test
-// are resolved together:
+// A warp owns 32 receivers x_j (one per lane) and walks a chunk of the
+// gather's Morton-ordered VPL copy (render.cu), one VPL at a time — or, with
+// VPL_GROUP > 1, in groups of nearby consecutive VPLs (measured slower at C4,
+// off).  For each VPL every lane computes the Eq. 1 cosine terms of its
+// receiver (exact fp32, O13), and the shadow segments x_j -> y that need a
+// visibility test are resolved together:
 //   1. occluder cache: exact MT tests against the lane's two latest occluders
-//      and the warp's latest one;
+//      and the warp's latest one, skipped by lanes whose last traced segment
+//      was visible;
 //   2. beam traversal of the 16-wide BVH (leaves = single triangles): all
 //      remaining segments lie in the beam {y + s*D : y in Ybox, D in Dbox,
 //      s in [s_lo, s_hi]}; lane c of each half-warp tests child c of a node
-//      against it (interval arithmetic, two nodes per step), hit inner
-//      children go on a warp-uniform shared-memory stack, hit triangles are
-//      tested at once by every lane against each of its pending segments
-//      with the exact MT of O9 (the terms that depend only on the origin and
-//      the triangle are shared between a lane's segments — same operations,
-//      same bits);
-//   3. loose beams (a D component changes sign, or the spread of D is large)
-//      are split into single-VPL beams, and loose single beams fall back to
-//      the per-ray packet traversal of the 4-wide BVH.
+//      against it (interval arithmetic, two nodes per step, branch-free node
+//      loads), hit inner children go on a warp-uniform shared-memory stack,
+//      hit triangles are tested at once by every lane with a pending segment
+//      with the exact MT of O9;
+//   3. loose beams (a D component changes sign, or the spread of D is more
+//      than 0.3 of the shortest segment) fall back to the per-ray packet
+//      traversal of the 4-wide BVH (with groups: first one beam per VPL).
 // Every lane's answer equals the exact any-hit of O9 for each of its
 // segments: the beam and the boxes are conservative (boxes padded at build
 // time), and extra MT tests cannot change an any-hit result.
