@@ -18,11 +18,13 @@ __global__ void k_gbuffer(SceneView sv, BvhView bv, TileMap tm, vpl_gpoint* __re
     gb[pix] = primary_hit(sv, bv, pix);
 }
 
-// a8 — Eq. 1 gather.  Persistent: each warp takes 8x4 pixel blocks
-// from an atomic queue; all lanes walk the VPL list in the same order, in
-// groups of nearby VPLs, so the shadow segments of a warp form a narrow beam
-// (gather.cuh).  fp32 two-level accumulation: a per-batch partial is folded
-// into the running total every 256 VPLs (groups never straddle a batch).
+// a8 — Eq. 1 gather.  Persistent: each warp takes work items —
+// an 8x4 pixel block x a chunk of the Morton-ordered VPL copy — from an
+// atomic queue; all lanes walk the chunk's VPLs in the same order, so the
+// shadow segments of a warp form a narrow beam (gather.cuh).  fp32 two-level
+// accumulation: a per-batch partial is folded into the chunk total every 256
+// VPLs; the chunk totals of a block are folded in chunk order by the warp
+// that finishes the block's last chunk.
 // VPL clusters: 32 consecutive VPLs of the Morton-ordered copy, bounded by
 // their position box and normal box (4 float4: ylo, yhi, nlo, nhi).  A lane
 // can trace some VPL of the cluster only if cx = n_x.(y - x) > 0 and
