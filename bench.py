@@ -152,10 +152,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one GPU per rank; VPLGI_BENCH_BACKEND=gloo + fewer GPUs than ranks is a functional
+    # check of the multi-rank path only (ranks share a GPU, timings are not scaling numbers)
+    backend = os.environ.get("VPLGI_BENCH_BACKEND", "nccl")
+    gpu = local % torch.cuda.device_count() if backend != "nccl" else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     V.load_library()
     s = scenegen.make_scene(args.config)
     W, H, tw, th = s.width, s.height, 16, 16
@@ -176,8 +183,8 @@ def run_ours(args):
 
     def step(counters=False):
         if world > 1:
-            # the frame is assembled by an in-place SUM reduce into rank 0's buffer, so its
-            # other ranks' tiles must start from zero every step
+            # the frame is assembled by an in-place SUM all-reduce, so every rank's buffer
+            # holds the other ranks' tiles afterwards: they must start from zero every step
             r.rgb.zero_()
             dist.broadcast(d_verts, 0)
             dist.broadcast(d_alb, 0)
@@ -203,7 +210,7 @@ def run_ours(args):
                                          stream=stream)
         ev["gather"][1].record(stream)
         if world > 1:
-            dist.reduce(r.rgb, 0, op=dist.ReduceOp.SUM)      # disjoint tiles: exact assembly
+            dist.all_reduce(r.rgb, op=dist.ReduceOp.SUM)     # disjoint tiles: exact assembly on every rank
         return r.rgb
 
     # pairs per step: front-hit pixels of the whole frame x VPLs
@@ -231,7 +238,7 @@ def run_ours(args):
 
     launches0 = V.launch_count()
     step_ms, gather_ms = [], []
-    with ClockSampler(local) as clk:
+    with ClockSampler(gpu) as clk:
         for _ in range(args.steps):
             flush.zero_()                                   # L2 flush between timed steps (untimed)
             if world > 1:

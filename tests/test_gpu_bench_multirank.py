@@ -1,0 +1,38 @@
+"""Functional check of bench.py's multi-rank path (broadcast of scene and
+VPLs, per-rank tile gather, all-reduce assembly, max-over-ranks timing,
+rank-0 JSON line): two ranks launched by torch.distributed.run share the one
+GPU of the test box over gloo (VPLGI_BENCH_BACKEND=gloo).  The ranks never
+wait on one another inside a kernel; the timings are not scaling numbers."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _run(n, port):
+    env = dict(os.environ, VPLGI_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), "--gpus", str(n),
+           "--steps", "1", "--warmup", "3", "--config", "1", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_two_ranks_match_one_rank_counts():
+    one, two = _run(1, 29531), _run(2, 29532)
+    assert two["n_gpus"] == 2 and two["config"]["parallelism"] == "pixel-tiles x2"
+    for k in ("pairs", "traced", "visible"):
+        assert two["counters"][k] == one["counters"][k], k      # the tiles of both ranks cover the frame once
+    assert two["config"]["hit_pixels"] == one["config"]["hit_pixels"]
+    assert two["value"] > 0 and two["e2e"]["value"] > 0
