@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstddef>
 #include <climits>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "../../include/vplgi.h"
@@ -28,6 +29,28 @@ int32_t check_arch();
     } while (0)
 #define VPL_CUDA(call) VPL_TRY(::vplgi::check_cuda((call), #call))
 #define VPL_LAUNCHED(name) VPL_TRY(::vplgi::check_launch(name))
+
+// Device-side bounds checks (stack depth, node / triangle / block indices),
+// compiled in with -DVPL_DEBUG=1 (tools/debug_checks.py builds that variant
+// and runs the parity tests on it); a failed check prints and traps, which
+// the next call reports as VPL_ECUDA.
+#ifndef VPL_DEBUG
+#define VPL_DEBUG 0
+#endif
+#if VPL_DEBUG
+#define VPL_DCHECK(c)                                                                   \
+    do {                                                                                \
+        if (!(c)) {                                                                     \
+            printf("VPL_DCHECK %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                  \
+            __trap();                                                                   \
+        }                                                                               \
+    } while (0)
+#else
+#define VPL_DCHECK(c) \
+    do {              \
+    } while (0)
+#endif
 
 // ------------------------------------------------------------------ layouts
 constexpr int kMaxLights = VPL_MAX_LIGHTS;
@@ -109,6 +132,7 @@ struct BvhView {
     const float4* wide;    // 16-wide nodes (cone traversal)
     const float4* wide4;   // 4-wide nodes (per-ray packet traversal)
     int32_t root;
+    int32_t n;             // triangles (bounds checks under VPL_DEBUG)
 };
 inline size_t bvh_layout(int64_t n, BvhHdr* h) {
     size_t off = align_up(sizeof(BvhHdr));
@@ -132,6 +156,7 @@ inline BvhView bvh_view(const void* blob, int64_t n) {
     v.wide = (const float4*)((const char*)blob + h.off_wide);
     v.wide4 = (const float4*)((const char*)blob + h.off_wide4);
     v.root = h.root;
+    v.n = (int32_t)n;
     return v;
 }
 
@@ -286,6 +311,7 @@ __device__ __forceinline__ bool bvh_any_hit(const BvhView& bv, const Ray& r, Tra
             int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
             if (h0 && h1) {
                 bool first0 = t0 <= t1;
+                VPL_DCHECK(sp < kStack);
                 stack[sp++] = first0 ? c1 : c0;
                 node = first0 ? c0 : c1;
                 continue;
@@ -325,6 +351,7 @@ __device__ __forceinline__ int bvh_closest(const BvhView& bv, const Ray& r, floa
             int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
             if (h0 && h1) {
                 bool first0 = t0 <= t1;
+                VPL_DCHECK(sp < kStack);
                 stack[sp++] = first0 ? c1 : c0;
                 node = first0 ? c0 : c1;
                 continue;
@@ -453,6 +480,7 @@ __device__ __forceinline__ bool warp_traverse_ray(const BvhView& bv, Ray r, bool
                 int first = (m & 1u) ? r0 : (m & 2u) ? r1 : (m & 4u) ? r2 : r3;
                 unsigned rest = m & (m - 1u);
                 // push the later hits, farthest first, so the next in order is on top
+                VPL_DCHECK(sp + 3 <= kWarpStack);
                 if (rest & 8u) sstack[sp++] = r3;
                 if (rest & 4u) sstack[sp++] = r2;
                 if (rest & 2u) sstack[sp++] = r1;
@@ -462,6 +490,7 @@ __device__ __forceinline__ bool warp_traverse_ray(const BvhView& bv, Ray r, bool
         } else {
             int first, count;
             leaf_range(node, first, count);
+            VPL_DCHECK(first >= 0 && count >= 1 && first + count <= bv.n);
             for (int k = 0; k < count; ++k) {
                 const float4* tr = bv.tris + 3 * (first + k);
                 float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);

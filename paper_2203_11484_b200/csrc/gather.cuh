@@ -223,6 +223,7 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
         sp = max(sp - 2, 0);
         // no branch: an empty half-step loads the root's children (cached) and masks the result
         const int nsafe = node >= 0 ? node : 0;
+        VPL_DCHECK(nsafe < (bv.n > 1 ? bv.n - 1 : 1));
         const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)nsafe << 9) + ((lane & (kWide - 1)) << 5));
         const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
         int ref = node >= 0 ? __float_as_int(lo.w) : INT_MIN;
@@ -251,12 +252,14 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
             if (hit && ref >= 0) sstack[sp + pos] = ref;
 #endif
             sp += nA + nB;
+            VPL_DCHECK(sp <= kWarpStack);
         }
         __syncwarp();
         while (Bl) {   // hit triangle children
             const int k = __ffs(Bl) - 1;
             Bl &= Bl - 1u;
             const int tri = ~__shfl_sync(0xFFFFFFFFu, ref, k) >> 3;
+            VPL_DCHECK(tri >= 0 && tri < bv.n);
             {   // no branch around the test: lanes with nothing pending are masked inside mt_segs
                 const float4* tr = bv.tris + 3 * tri;
                 const unsigned h = mt_segs<kCount>(x, S, S.pend, tmin, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), st);

@@ -162,6 +162,8 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             }
         }
         const int64_t blk = n_chunks > 1 ? tm.block_index(g / n_chunks) : -1;
+        VPL_DCHECK(blk < (int64_t)((tm.W + 7) / 8) * ((tm.H + 3) / 4));
+        VPL_DCHECK(pix < (int64_t)tm.W * tm.H);
         if (blk >= 0) {
             // chunk partial sums, (block, chunk, lane)-contiguous; the warp that completes a block's last
             // chunk folds them in chunk order (fp32) while they are still in L2, writes the pixels and
@@ -458,7 +460,7 @@ static size_t gather_layout(int32_t M, int32_t W, int32_t H, char* base, GatherW
 
 static int32_t make_tilemap(const SceneHdr& hh, const int32_t* d_tiles, int32_t n_tiles, int32_t tw, int32_t th,
                             TileMap* tm) {
-    if (!d_tiles || n_tiles < 0 || tw <= 0 || th <= 0 || tw % 8 || th % 4) {
+    if ((!d_tiles && n_tiles != 0) || n_tiles < 0 || tw <= 0 || th <= 0 || tw % 8 || th % 4) {
         set_error("bad tile arguments (tile_w %% 8 == 0, tile_h %% 4 == 0 required)");
         return VPL_EINVAL;
     }

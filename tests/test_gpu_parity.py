@@ -220,6 +220,19 @@ def test_empty_vpl_list_is_black(gpu, scenes):
     assert float(rgb.abs().max()) == 0.0
 
 
+def test_empty_tile_list_writes_nothing(gpu, scenes):
+    """n_tiles = 0 (a rank with no tiles): every per-tile call is a no-op
+    (include/vplgi.h), also when the empty tile tensor has a null data pointer."""
+    s = scenes[1]
+    gb, tiles = gpu[1].gbuffer()
+    v, _ = gpu[1].generate()
+    none = torch.zeros(0, dtype=torch.int32, device="cuda")
+    rgb = torch.full((s.height * s.width * 3,), 7.0, device="cuda")
+    V.gather_indirect(gpu[1].scene, gpu[1].bvh, gb, v, none, s.width, s.height, rgb=rgb)
+    V.render_direct(gpu[1].scene, gpu[1].bvh, gb, none, s.width, s.height, rgb=rgb, accumulate=True)
+    assert bool((rgb == 7.0).all())
+
+
 def test_single_triangle_scene():
     V_ = np.array([[[-1, 0, -1], [-1, 0, 1], [1, 0, -1]]], np.float32)
     s = scenegen.custom_scene(V_, np.full((1, 3), 0.5), scenegen.make_light([0, 1.999, 0]),
