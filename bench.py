@@ -103,7 +103,7 @@ OPS = {"pairs": (18, 3, 0),       # d (3), r^2 (5), cx (5), ci (5) | tri, cx, ci
        "traced": (6, 2, 4),       # tmax, cx*ci, r2*max, 3 FFMA | test, max | sqrt, 3 div (direction)    (O9, O13)
        "box_tests": (12, 5, 0),   # per-ray slab (centre/half-extent): 3 FFMA + 3 FMUL + 6 FADD | 4 min/max + cmp
        "cone_tests": (6, 11, 0),  # beam x child box: 6 FFMA | 6 SEL + 4 min/max + 1 cmp (gather.cuh beam_box)
-       "tri_tests": (44, 7, 1)}   # exact Moller-Trumbore (O9): 44 FMUL/FADD | 7 compares | 1 division
+       "tri_tests": (44, 9, 0)}   # exact MT any hit (O9, R25): 41 products/sums + a_u+a_v, tmin*D, tmax*D | 6 compares + 3 sign flips
 
 # Pipe rates in thread-ops per clock per SM, measured on this pool's B200
 # (tools/pipebench.cu, profiles/r01_pipebench.jsonl): FFMA/FMUL/FADD 126,

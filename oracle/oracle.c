@@ -180,7 +180,11 @@ void oracle_tri_data(const OScene* s, float* nrm, float* cen, float* area, uint6
 
 /* ------------------------------------------------------------------------ */
 /* O9 — Moller-Trumbore, brute force over every triangle.                    */
-/* hit(i) <=> det != 0 & u>=0 & u<=1 & v>=0 & u+v<=1 & tmin<t & t<tmax       */
+/* closest hit: u = a_u/det, v = a_v/det, t = a_t/det (inv = 1/det),        */
+/*   hit(i) <=> det != 0 & u>=0 & u<=1 & v>=0 & u+v<=1 & tmin<t & t<tmax    */
+/* any hit (V of Eq. 1, reading R25): the same predicate without the        */
+/* division — a_u, a_v, a_t sign-normalised by det (exact negations), D=|det|*/
+/*   hit(i) <=> a_u>=0 & a_u<=D & a_v>=0 & a_u+a_v<=D & a_t>tmin*D & a_t<tmax*D */
 /* ------------------------------------------------------------------------ */
 #define CHUNK 2048
 
@@ -193,16 +197,16 @@ static int any_hit_chunk(const OScene* s, f3 o, f3 d, float tmin, float tmax, in
         float pvy = d.z * e2x - d.x * e2z;
         float pvz = d.x * e2y - d.y * e2x;
         float det = (e1x * pvx + e1y * pvy) + e1z * pvz;
-        float inv = 1.0f / det;
         float sx = o.x - s->v0x[i], sy = o.y - s->v0y[i], sz = o.z - s->v0z[i];
-        float u = ((sx * pvx + sy * pvy) + sz * pvz) * inv;
+        float au = (sx * pvx + sy * pvy) + sz * pvz;
         float qx = sy * e1z - sz * e1y;
         float qy = sz * e1x - sx * e1z;
         float qz = sx * e1y - sy * e1x;
-        float v = ((d.x * qx + d.y * qy) + d.z * qz) * inv;
-        float t = ((e2x * qx + e2y * qy) + e2z * qz) * inv;
-        int h = (det != 0.0f) & (u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) &
-                (t > tmin) & (t < tmax);
+        float av = (d.x * qx + d.y * qy) + d.z * qz;
+        float at = (e2x * qx + e2y * qy) + e2z * qz;
+        if (det < 0.0f) { au = -au; av = -av; at = -at; }   /* sign-normalise (exact) */
+        float D = fabsf(det);
+        int h = (au >= 0.0f) & (au <= D) & (av >= 0.0f) & ((au + av) <= D) & (at > tmin * D) & (at < tmax * D);
         hit |= h;
     }
     return hit;

@@ -274,6 +274,23 @@ __device__ __forceinline__ bool mt_hit(f3 o, f3 d, float4 a, float4 b, float4 c,
     return (det != 0.0f) & (u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) & (t > tmin) & (t < tmax);
 }
 
+// O9 any hit (the V of Eq. 1), division-free (reading R25): the closest-hit
+// predicate above with u, v, t scaled by |det| — a_u, a_v, a_t sign-normalised
+// by det (exact negations), compared with |det|, tmin*|det|, tmax*|det|.
+__device__ __forceinline__ bool mt_any(f3 o, f3 d, float4 a, float4 b, float4 c, float tmin, float tmax) {
+    f3 v0 = xyz(a), e1 = xyz(b), e2 = xyz(c);
+    f3 pv = cross(d, e2);
+    float det = dot(e1, pv);
+    const unsigned sg = __float_as_uint(det) & 0x80000000u;
+    const float adet = fabsf(det);
+    f3 s = o - v0;
+    float u = __uint_as_float(__float_as_uint(dot(s, pv)) ^ sg);
+    f3 q = cross(s, e1);
+    float v = __uint_as_float(__float_as_uint(dot(d, q)) ^ sg);
+    float t = __uint_as_float(__float_as_uint(dot(e2, q)) ^ sg);
+    return (u >= 0.0f) & (u <= adet) & (v >= 0.0f) & ((u + v) <= adet) & (t > tmin * adet) & (t < tmax * adet);
+}
+
 struct TravStats {
     uint32_t boxes = 0, tris = 0;
     uint32_t wrays = 0, wsteps = 0;  // warp-level packets / iterations (counted on lane 0)
@@ -323,9 +340,8 @@ __device__ __forceinline__ bool bvh_any_hit(const BvhView& bv, const Ray& r, Tra
             leaf_range(node, first, count);
             for (int k = 0; k < count; ++k) {
                 const float4* tr = bv.tris + 3 * (first + k);
-                float t;
                 if (kCount) st->tris += 1;
-                if (mt_hit(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax, t)) return true;
+                if (mt_any(r.o, r.d, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), r.tmin, r.tmax)) return true;
             }
         }
         if (sp == 0) return false;
@@ -494,8 +510,7 @@ __device__ __forceinline__ bool warp_traverse_ray(const BvhView& bv, Ray r, bool
             for (int k = 0; k < count; ++k) {
                 const float4* tr = bv.tris + 3 * (first + k);
                 float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
-                float t;
-                bool hit = mt_hit(r.o, r.d, a, b, c, r.tmin, r.tmax, t) & go & !occl;
+                bool hit = mt_any(r.o, r.d, a, b, c, r.tmin, r.tmax) & go & !occl;
                 if (kCount && go && !occl) st->tris += 1;
                 if (hit) { occl = true; cache.found(first + k); }
             }

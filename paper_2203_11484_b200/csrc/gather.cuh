@@ -92,7 +92,7 @@ struct Segs {
 
 // exact MT (O9) of the pending segments of one lane against one triangle;
 // the origin-only terms s = x - v0, q = s x e1, e2.q are shared (identical
-// operations to mt_hit, so identical bits)
+// operations to mt_any, so identical bits)
 template <bool kCount>
 __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, float tmin, float4 a, float4 b,
                                             float4 c, TravStats* st) {
@@ -108,12 +108,15 @@ __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, 
             const f3 d = S.d[k];
             const f3 pv = cross(d, e2);
             const float det = dot(e1, pv);
-            const float inv = 1.0f / det;
-            const float u = dot(s, pv) * inv;
-            const float v = dot(d, q) * inv;
-            const float t = tq * inv;
-            // (det == 0 needs no test of its own: u is then NaN or +-inf and fails u >= 0 or u <= 1)
-            if ((u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) & (t > tmin) & (t < S.tmax[k]))
+            // O9 any hit, division-free (reading R25): sign-normalised by det (exact negations)
+            const unsigned sg = __float_as_uint(det) & 0x80000000u;
+            const float adet = fabsf(det);
+            const float u = __uint_as_float(__float_as_uint(dot(s, pv)) ^ sg);
+            const float v = __uint_as_float(__float_as_uint(dot(d, q)) ^ sg);
+            const float t = __uint_as_float(__float_as_uint(tq) ^ sg);
+            // (det = +-0 or NaN: t > tmin*|det| and t < tmax*|det| cannot both hold)
+            if ((u >= 0.0f) & (u <= adet) & (v >= 0.0f) & ((u + v) <= adet) & (t > tmin * adet) &
+                (t < S.tmax[k] * adet))
                 hit |= 1u << k;
         }
     }
