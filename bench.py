@@ -100,7 +100,7 @@ class ClockSampler:
 # Moller-Trumbore, so those count as separate FMUL/FADD; square roots and
 # divisions count as one MUFU op each.  (fma, alu, mufu) per unit:
 OPS = {"pairs": (18, 3, 0),       # d (3), r^2 (5), cx (5), ci (5) | tri, cx, ci tests                 (O13)
-       "traced": (6, 2, 4),       # tmax, cx*ci, r2*max, 3 FFMA | test, max | sqrt, 3 div (direction)    (O9, O13)
+       "traced": (9, 2, 2),       # tmax, cx*ci, r2*max, 3 FFMA, d*inv (3) | test, max | sqrt, 1/dist  (O9, O13, R25)
        "box_tests": (12, 5, 0),   # per-ray slab (centre/half-extent): 3 FFMA + 3 FMUL + 6 FADD | 4 min/max + cmp
        "cone_tests": (6, 11, 0),  # beam x child box: 6 FFMA | 6 SEL + 4 min/max + 1 cmp (gather.cuh beam_box)
        "tri_tests": (44, 9, 0)}   # exact MT any hit (O9, R25): 41 products/sums + a_u+a_v, tmin*D, tmax*D | 6 compares + 3 sign flips

@@ -272,7 +272,8 @@ static int64_t closest_hit(const OScene* s, f3 o, f3 d, float tmin, float tmax, 
 static int occluded(const OScene* s, f3 a, f3 b) {
     f3 d = sub(b, a);
     float dist = sqrtf(dot(d, d));
-    f3 dir = mk(d.x / dist, d.y / dist, d.z / dist);
+    float inv = 1.0f / dist;                       /* R25: one division, three products */
+    f3 dir = mk(d.x * inv, d.y * inv, d.z * inv);
     float tmin = s->eps, tmax = dist - s->eps;
     if (!(tmax > tmin)) return 0;
     return any_hit(s, a, dir, tmin, tmax);

@@ -403,7 +403,8 @@ __device__ __forceinline__ bool seg_ray(f3 a, f3 b, float eps, Ray& r) {
     f3 d = b - a;
     float dist = sqrtf(dot(d, d));
     r.o = a;
-    r.d = mk3(d.x / dist, d.y / dist, d.z / dist);
+    const float inv = 1.0f / dist;   // R25: dir = d * (1/dist)
+    r.d = mk3(d.x * inv, d.y * inv, d.z * inv);
     r.tmin = eps;
     r.tmax = dist - eps;
     return r.tmax > r.tmin;

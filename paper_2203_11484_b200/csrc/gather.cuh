@@ -375,7 +375,8 @@ __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_rec
                 traced |= 1u << k;
                 w[k] = __fdividef(cx * ci, r2 * fmaxf(r2, b2));
                 const float dist = sqrtf(r2);   // = sqrtf(dot(d, d)) of O9's segment setup
-                S.d[k] = mk3(d.x / dist, d.y / dist, d.z / dist);
+                const float inv = 1.0f / dist;  // R25: dir = d * (1/dist)
+                S.d[k] = mk3(d.x * inv, d.y * inv, d.z * inv);
                 S.tmax[k] = dist - eps;
                 if (S.tmax[k] > eps) S.pend |= 1u << k;
             }
