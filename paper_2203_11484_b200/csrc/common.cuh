@@ -435,6 +435,18 @@ struct OccluderCache {
     }
 };
 
+// warp-wide float min / max (redux.sync .f32, sm_100a): all 32 lanes take part
+__device__ __forceinline__ float warp_min_f32(float v) {
+    float r;
+    asm volatile("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+    return r;
+}
+__device__ __forceinline__ float warp_max_f32(float v) {
+    float r;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+    return r;
+}
+
 __device__ __forceinline__ int fkey(float f) {   // order-preserving float -> int
     int i = __float_as_int(f);
     return i ^ ((i >> 31) & 0x7FFFFFFF);

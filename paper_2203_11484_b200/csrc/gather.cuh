@@ -163,13 +163,12 @@ __device__ __forceinline__ bool make_beam(f3 x, const f3* yk, unsigned want, uns
     }
     float Dn[3], Dm[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        Dn[a] = fkey_inv(__reduce_min_sync(0xFFFFFFFFu, fkey(dn[a])));
-        Dm[a] = fkey_inv(__reduce_max_sync(0xFFFFFFFFu, fkey(dm[a])));
+    for (int a = 0; a < 3; ++a) {   // sm_100a float warp reductions (CREDUX, result in a uniform register)
+        Dn[a] = warp_min_f32(dn[a]);
+        Dm[a] = warp_max_f32(dm[a]);
     }
-    // l2 >= 0: int order = float order
-    const float lmin = sqrtf(__int_as_float(__reduce_min_sync(0xFFFFFFFFu, __float_as_int(l2n))));
-    const float lmax = sqrtf(__int_as_float(__reduce_max_sync(0xFFFFFFFFu, __float_as_int(l2m))));
+    const float lmin = sqrtf(warp_min_f32(l2n));
+    const float lmax = sqrtf(warp_max_f32(l2m));
     const float spread = fmax3(Dm[0] - Dn[0], Dm[1] - Dn[1], Dm[2] - Dn[2]);
     bool tight = spread < kConeSpread * lmin;
     B.pos = 0;
