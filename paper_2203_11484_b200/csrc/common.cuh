@@ -288,7 +288,8 @@ __device__ __forceinline__ bool mt_any(f3 o, f3 d, float4 a, float4 b, float4 c,
     f3 q = cross(s, e1);
     float v = __uint_as_float(__float_as_uint(dot(d, q)) ^ sg);
     float t = __uint_as_float(__float_as_uint(dot(e2, q)) ^ sg);
-    return (u >= 0.0f) & (u <= adet) & (v >= 0.0f) & ((u + v) <= adet) & (t > tmin * adet) & (t < tmax * adet);
+    // u <= |det| is implied by v >= 0 and RN(u + v) <= |det| (see mt_segs)
+    return (u >= 0.0f) & (v >= 0.0f) & ((u + v) <= adet) & (t > tmin * adet) & (t < tmax * adet);
 }
 
 struct TravStats {

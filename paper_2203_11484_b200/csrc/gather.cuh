@@ -114,9 +114,10 @@ __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, 
             const float u = __uint_as_float(__float_as_uint(dot(s, pv)) ^ sg);
             const float v = __uint_as_float(__float_as_uint(dot(d, q)) ^ sg);
             const float t = __uint_as_float(__float_as_uint(tq) ^ sg);
-            // (det = +-0 or NaN: t > tmin*|det| and t < tmax*|det| cannot both hold)
-            if ((u >= 0.0f) & (u <= adet) & (v >= 0.0f) & ((u + v) <= adet) & (t > tmin * adet) &
-                (t < S.tmax[k] * adet))
+            // (det = +-0 or NaN: t > tmin*|det| and t < tmax*|det| cannot both hold.  O9's u <= |det|
+            // is implied: v >= 0 makes RN(u + v) >= u, so RN(u + v) <= |det| gives u <= |det|; a NaN
+            // u or v fails the other tests)
+            if ((u >= 0.0f) & (v >= 0.0f) & ((u + v) <= adet) & (t > tmin * adet) & (t < S.tmax[k] * adet))
                 hit |= 1u << k;
         }
     }
@@ -324,10 +325,12 @@ __device__ __forceinline__ void resolve_group(const BvhView& bv, f3 x, Segs& S, 
 // The VPL group starting at i (uniform): the longest run of <= kGroup VPLs in
 // [i, iend) whose position box stays within kGroupTol x the distance from
 // the first VPL to the warp's reference receiver xr.
-__device__ __forceinline__ int group_at(const vpl_record* __restrict__ vpls, int i, int iend, f3 xr, f3* yk) {
+__device__ __forceinline__ int group_at(const vpl_record* __restrict__ vpls, int i, int iend, f3 xr, f3* yk,
+                                        int* yt) {
     const float4* p = (const float4*)(vpls + i);
     float4 a = __ldg(p);
     yk[0] = xyz(a);
+    yt[0] = __float_as_int(a.w);   // the VPL's triangle (record field tri)
     f3 lo = yk[0], hi = yk[0];
     f3 dr = yk[0] - xr;
     const float lim = kGroupTol * sqrtf(dot(dr, dr));
@@ -340,7 +343,7 @@ __device__ __forceinline__ int group_at(const vpl_record* __restrict__ vpls, int
             f3 l2 = mk3(fminf(lo.x, y.x), fminf(lo.y, y.y), fminf(lo.z, y.z));
             f3 h2 = mk3(fmaxf(hi.x, y.x), fmaxf(hi.y, y.y), fmaxf(hi.z, y.z));
             if (fmax3(h2.x - l2.x, h2.y - l2.y, h2.z - l2.z) < lim) {
-                yk[k] = y; lo = l2; hi = h2; g = k + 1;
+                yk[k] = y; yt[k] = __float_as_int(b.w); lo = l2; hi = h2; g = k + 1;
             }
         }
     }
@@ -348,13 +351,14 @@ __device__ __forceinline__ int group_at(const vpl_record* __restrict__ vpls, int
 }
 
 // One group for one lane: Eq. 1 terms (O13, exact fp32 order), segment
-// setup (O9), cache, traversal.  Returns the traced mask; *vis = traced and
+// setup (O9), cache, traversal.  Returns traced | vis << 16: the traced mask and vis = traced and
 // unoccluded; w[k] = cx*ci / (r2 * max(r2, b2)) for the visible ones.
 template <bool kCount>
 __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_record* __restrict__ vpls, int i, int g,
-                                                const f3* yk, f3 x, f3 nx, int tri_x, bool active, float eps,
+                                                const f3* yk, const int* yt, f3 x, f3 nx, int tri_x, bool active,
+                                                float eps,
                                                 float b2, OccluderCache& cache, int* __restrict__ sstack,
-                                                TravStats* st, unsigned* vis, float* w) {
+                                                TravStats* st, float* w) {
     Segs S;
     S.pend = 0; S.occ = 0;
     unsigned traced = 0;
@@ -365,7 +369,7 @@ __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_rec
         S.tmax[k] = 0.0f;
         if (k < g) {
             const float4 nb = __ldg((const float4*)(vpls + i + k) + 1);
-            const int tri_i = __float_as_int(__ldg((const float*)(vpls + i + k) + 3));
+            const int tri_i = yt[k];
             const f3 d = yk[k] - x;
             const float r2 = dot(d, d);
             const float cx = dot(nx, d);
@@ -381,7 +385,6 @@ __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_rec
             }
         }
     }
-    *vis = 0;
     if (!__any_sync(0xFFFFFFFFu, traced != 0)) return 0;
     // occluder cache: exact MT against recent occluders
     const uint32_t t0 = kCount ? st->tris : 0;
@@ -401,11 +404,11 @@ __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_rec
 #endif
     if (kCount) { st->chits += __popc(S.occ); st->ctests += st->tris - t0; }
     resolve_group<kCount>(bv, x, S, eps, yk, g, cache, sstack, st);
-    *vis = traced & ~S.occ;
+    const unsigned vis = traced & ~S.occ;
 #if VPL_CACHE_STREAK
-    if (traced) cache.vis_streak = (*vis == traced);
+    if (traced) cache.vis_streak = (vis == traced);
 #endif
-    return traced;
+    return traced | vis << 16;
 }
 
 }  // namespace vplgi

@@ -130,11 +130,12 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                     const int c1 = min(c0 + kCluster, i1);
                     for (int i = c0; i < c1;) {
                         f3 yk[kGroup];
-                        const int gsz = group_at(vpls, i, c1, xr, yk);
-                        unsigned vis;
+                        int yt[kGroup];
+                        const int gsz = group_at(vpls, i, c1, xr, yk, yt);
                         float w[kGroup];
-                        const unsigned tr = shade_group<kCount>(bv, vpls, i, gsz, yk, x, nx, tri_x, active, eps, b2,
-                                                                cache, sstack, &st, &vis, w);
+                        const unsigned tv = shade_group<kCount>(bv, vpls, i, gsz, yk, yt, x, nx, tri_x, active, eps, b2,
+                                                                cache, sstack, &st, w);
+                        const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
                         if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
 #pragma unroll
                         for (int k = 0; k < kGroup; ++k) {
@@ -237,11 +238,12 @@ __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict
         const int i0 = (int)(wd * 32), i1 = min(M, i0 + 32);
         for (int i = i0; i < i1;) {
             f3 yk[kGroup];
-            const int gsz = group_at(vpls, i, i1, xr, yk);
-            unsigned vis;
+            int yt[kGroup];
+            const int gsz = group_at(vpls, i, i1, xr, yk, yt);
             float w[kGroup];
-            const unsigned tr = shade_group<false>(bv, vpls, i, gsz, yk, x, nx, tri_x, active, eps, b2, cache, sstack,
-                                                   nullptr, &vis, w);
+            const unsigned tv = shade_group<false>(bv, vpls, i, gsz, yk, yt, x, nx, tri_x, active, eps, b2, cache, sstack,
+                                                   nullptr, w);
+            const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
             tb |= tr << (i - i0);
             vb |= vis << (i - i0);
             i += gsz;
