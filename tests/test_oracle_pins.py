@@ -759,3 +759,49 @@ def test_metropolis_is_unbiased_in_power():
         sums.append(out["flux"][:, 0].astype(np.float64).sum())
     m, se = np.mean(sums), np.std(sums) / math.sqrt(len(sums))
     assert abs(m - tot) < 4 * se + 1e-3 * tot, (m, tot, se)
+
+
+def test_any_hit_division_free_matches_float64_segment_triangle():
+    """R25 pin: the division-free any-hit of O9 (u, v, t scaled by |det|,
+    sign-normalised by det) against a float64 segment-triangle test written
+    from geometry (plane crossing point + barycentric coordinates), on random
+    segments through one triangle from BOTH sides (det > 0 and det < 0),
+    skipping cases within a margin of an edge or of the eps-shrunk ends."""
+    T = np.array([[[0.2, 0.1, 0.3], [1.7, 0.4, 0.2], [0.6, 1.5, 1.1]]], np.float32)
+    s = scenegen.custom_scene(T, np.full((1, 3), 0.5), scenegen.make_light([0.5, 1.9, 0.5]),
+                              scenegen.make_camera([0.5, 0.8, -2.0], [0.5, 0.5, 0.5], 60, 8, 8), 8, 8,
+                              M=4, K_near=4, max_depth=1, rr=1, seed=1, T=5.0)
+    o = oracle.OracleScene(s)
+    eps = float(o.consts()[1])
+    v0, v1, v2 = (T[0, i].astype(np.float64) for i in range(3))
+    n = np.cross(v1 - v0, v2 - v0)
+    rng = np.random.default_rng(25)
+    checked = {True: 0, False: 0}
+    sides = set()
+    for _ in range(4000):
+        a = rng.uniform(-0.5, 2.2, 3).astype(np.float32)
+        b = rng.uniform(-0.5, 2.2, 3).astype(np.float32)
+        A, B = a.astype(np.float64), b.astype(np.float64)
+        d = B - A
+        L = np.linalg.norm(d)
+        if L < 4 * eps:
+            continue
+        den = n @ d
+        if abs(den) < 1e-3 * np.linalg.norm(n) * L:
+            continue                                   # nearly parallel: no margin
+        t = (n @ (v0 - A)) / den                      # crossing at A + t d
+        p = A + t * d
+        # barycentrics of p
+        m = np.array([v1 - v0, v2 - v0]).T
+        uv, *_ = np.linalg.lstsq(m, p - v0, rcond=None)
+        u, w = uv
+        bary_margin = min(u, w, 1 - u - w)
+        end_margin = min(t * L - eps, (1 - t) * L - eps)
+        if abs(bary_margin) < 1e-4 or abs(end_margin) < 1e-4:
+            continue
+        hit = bary_margin > 0 and end_margin > 0
+        assert o.occluded(a, b) == hit, (a, b, bary_margin, end_margin)
+        checked[hit] += 1
+        if hit:
+            sides.add(bool(den > 0))
+    assert checked[True] > 100 and checked[False] > 1000 and sides == {True, False}
