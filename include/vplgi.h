@@ -161,10 +161,11 @@ VPL_API int32_t vpl_scene_consts(const void* d_scene, double* diag, float* eps, 
 
 /* -------------------------------------------------------------------- */
 /* a2  build_bvh (the paper has no acceleration structure)
- * Deterministic LBVH (Karras 2012): 63-bit Morton codes of centroids over
- * the scene bbox, radix sort (code, index), hierarchy from the highest
- * differing bit, bottom-up AABB refit padded by 2^-16 * max|coord| so the
- * box test is conservative w.r.t. the exact Moller-Trumbore test (O9).
+ * Deterministic PLOC build (search radius 64) over the 63-bit Morton order
+ * of the centroids, SAH leaf collapse, then a 16-wide (beam traversal) and a
+ * 4-wide (per-ray traversal) collapse of the same tree; boxes padded by
+ * 2^-16 * max|coord| so every box test is conservative w.r.t. the exact
+ * Moller-Trumbore tests of O9.  Same scene in, same bytes out.
  * d_bvh: vpl_bvh_bytes(...).bvh bytes; d_work: .work bytes (scratch). */
 VPL_API int32_t vpl_bvh_bytes(int64_t n_tris, size_t* bvh_bytes, size_t* work_bytes);
 VPL_API int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* d_work, size_t work_bytes,
@@ -291,7 +292,8 @@ VPL_API int32_t vpl_visibility_dump(const void* d_scene, const void* d_bvh, cons
 /* closest hit of n rays (o, dir float[n*3]) in (tmin, tmax): d_tri int32 (-1 miss), d_t float */
 VPL_API int32_t vpl_closest_hit_batch(const void* d_scene, const void* d_bvh, const float* d_o, const float* d_dir,
                               int64_t n, float tmin, float tmax, int32_t* d_tri, float* d_t, void* stream);
-/* segment occlusion of n point pairs (O9 unoccluded): d_occ uint8 */
+/* segment occlusion of n point pairs (O9 unoccluded: eps-shrunk segment,
+ * division-free any hit of DESIGN.md R25): d_occ uint8 */
 VPL_API int32_t vpl_occluded_batch(const void* d_scene, const void* d_bvh, const float* d_a, const float* d_b,
                            int64_t n, uint8_t* d_occ, void* stream);
 /* Philox4x32-10 of n (ctr, key) pairs: d_in uint32[n*6], d_out uint32[n*4] */
