@@ -204,6 +204,7 @@ VPL_API int32_t vpl_render_gbuffer(const void* d_scene, const void* d_bvh, const
 /* a8  gather_indirect (Eq. 1; O13): indirect-only linear radiance
  * d_rgb float[H*W*3] for the listed tiles (others untouched).  Miss or
  * back-face pixels get 0.  d_ctr (nullable) accumulates counters.
+ * n_tiles = 0 is a no-op (d_tiles may then be null), as for every per-tile call.
  * d_work: vpl_gather_bytes(n_vpls, W, H) bytes (tile queue, a Morton-ordered
  * copy of the VPLs — Eq. 1 is a sum over the set, the gather visits it in
  * spatial order; the caller's array is not modified — VPL cluster bounds and,
