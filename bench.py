@@ -96,14 +96,15 @@ class ClockSampler:
 # ---------------------------------------------------------------------------- algorithmic op counts
 # Per-unit thread-op counts: the arithmetic the method itself prescribes per
 # unit of work, split by the SM pipe that executes it.  The
-# exact fp32 contract (O0) forbids FMA contraction in the Eq. 1 terms and in
-# Moller-Trumbore, so those count as separate FMUL/FADD; square roots and
-# divisions count as one MUFU op each.  (fma, alu, mufu) per unit:
+# exact fp32 contract (O0) forbids FMA contraction in the Eq. 1 terms and the
+# segment setup, so those count as separate FMUL/FADD; the any-hit MT counts
+# the fused form of reading R26; square roots and divisions count as one MUFU
+# op each.  (fma, alu, mufu) per unit:
 OPS = {"pairs": (18, 3, 0),       # d (3), r^2 (5), cx (5), ci (5) | tri, cx, ci tests                 (O13)
        "traced": (9, 2, 2),       # tmax, cx*ci, r2*max, 3 FFMA, d*inv (3) | test, max | sqrt, 1/dist  (O9, O13, R25)
        "box_tests": (12, 5, 0),   # per-ray slab (centre/half-extent): 3 FFMA + 3 FMUL + 6 FADD | 4 min/max + cmp
        "cone_tests": (6, 11, 0),  # beam x child box: 6 FFMA | 6 SEL + 4 min/max + 1 cmp (gather.cuh beam_box)
-       "tri_tests": (44, 9, 0)}   # exact MT any hit (O9, R25): 41 products/sums + a_u+a_v, tmin*D, tmax*D | 6 compares + 3 sign flips
+       "tri_tests": (30, 9, 0)}   # exact MT any hit (O9, R25, R26): 27 FMUL/FFMA/FADD + a_u+a_v, tmin*D, tmax*D | 6 compares + 3 sign flips
 
 # Pipe rates in thread-ops per clock per SM, measured on this pool's B200
 # (tools/pipebench.cu, profiles/r01_pipebench.jsonl): FFMA/FMUL/FADD 126,

@@ -184,6 +184,9 @@ void oracle_tri_data(const OScene* s, float* nrm, float* cen, float* area, uint6
 /*   hit(i) <=> det != 0 & u>=0 & u<=1 & v>=0 & u+v<=1 & tmin<t & t<tmax    */
 /* any hit (V of Eq. 1, reading R25): the same predicate without the        */
 /* division — a_u, a_v, a_t sign-normalised by det (exact negations), D=|det|*/
+/* — and its cross and dot products as fused multiply-adds (R26):           */
+/*   cross(a,b).x = fma(a.y, b.z, -(a.z*b.y)) (cyclic), dot(a,b) =          */
+/*   fma(a.z, b.z, fma(a.y, b.y, a.x*b.x))                                  */
 /*   hit(i) <=> a_u>=0 & a_u<=D & a_v>=0 & a_u+a_v<=D & a_t>tmin*D & a_t<tmax*D */
 /* ------------------------------------------------------------------------ */
 #define CHUNK 2048
@@ -193,17 +196,18 @@ static int any_hit_chunk(const OScene* s, f3 o, f3 d, float tmin, float tmax, in
     for (int64_t i = i0; i < i1; i++) {
         float e1x = s->e1x[i], e1y = s->e1y[i], e1z = s->e1z[i];
         float e2x = s->e2x[i], e2y = s->e2y[i], e2z = s->e2z[i];
-        float pvx = d.y * e2z - d.z * e2y;
-        float pvy = d.z * e2x - d.x * e2z;
-        float pvz = d.x * e2y - d.y * e2x;
-        float det = (e1x * pvx + e1y * pvy) + e1z * pvz;
+        /* R26: fused multiply-adds in the stated order (fmaf is IEEE fma, one rounding) */
+        float pvx = fmaf(d.y, e2z, -(d.z * e2y));
+        float pvy = fmaf(d.z, e2x, -(d.x * e2z));
+        float pvz = fmaf(d.x, e2y, -(d.y * e2x));
+        float det = fmaf(e1z, pvz, fmaf(e1y, pvy, e1x * pvx));
         float sx = o.x - s->v0x[i], sy = o.y - s->v0y[i], sz = o.z - s->v0z[i];
-        float au = (sx * pvx + sy * pvy) + sz * pvz;
-        float qx = sy * e1z - sz * e1y;
-        float qy = sz * e1x - sx * e1z;
-        float qz = sx * e1y - sy * e1x;
-        float av = (d.x * qx + d.y * qy) + d.z * qz;
-        float at = (e2x * qx + e2y * qy) + e2z * qz;
+        float au = fmaf(sz, pvz, fmaf(sy, pvy, sx * pvx));
+        float qx = fmaf(sy, e1z, -(sz * e1y));
+        float qy = fmaf(sz, e1x, -(sx * e1z));
+        float qz = fmaf(sx, e1y, -(sy * e1x));
+        float av = fmaf(d.z, qz, fmaf(d.y, qy, d.x * qx));
+        float at = fmaf(e2z, qz, fmaf(e2y, qy, e2x * qx));
         if (det < 0.0f) { au = -au; av = -av; at = -at; }   /* sign-normalise (exact) */
         float D = fabsf(det);
         int h = (au >= 0.0f) & (au <= D) & (av >= 0.0f) & ((au + av) <= D) & (at > tmin * D) & (at < tmax * D);

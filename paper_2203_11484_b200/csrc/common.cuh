@@ -277,17 +277,25 @@ __device__ __forceinline__ bool mt_hit(f3 o, f3 d, float4 a, float4 b, float4 c,
 // O9 any hit (the V of Eq. 1), division-free (reading R25): the closest-hit
 // predicate above with u, v, t scaled by |det| — a_u, a_v, a_t sign-normalised
 // by det (exact negations), compared with |det|, tmin*|det|, tmax*|det|.
+// The any-hit products are fused multiply-adds in a fixed order (reading R26):
+// cross(a,b).x = fma(a.y, b.z, -(a.z*b.y)) (cyclic), dot(a,b) = fma(a.z, b.z,
+// fma(a.y, b.y, a.x*b.x)) — one IEEE rounding per fma, identical in the oracle.
+__device__ __forceinline__ float dot_fma(f3 a, f3 b) { return __fmaf_rn(a.z, b.z, __fmaf_rn(a.y, b.y, a.x * b.x)); }
+__device__ __forceinline__ f3 cross_fma(f3 a, f3 b) {
+    return f3{__fmaf_rn(a.y, b.z, -(a.z * b.y)), __fmaf_rn(a.z, b.x, -(a.x * b.z)), __fmaf_rn(a.x, b.y, -(a.y * b.x))};
+}
+
 __device__ __forceinline__ bool mt_any(f3 o, f3 d, float4 a, float4 b, float4 c, float tmin, float tmax) {
     f3 v0 = xyz(a), e1 = xyz(b), e2 = xyz(c);
-    f3 pv = cross(d, e2);
-    float det = dot(e1, pv);
+    f3 pv = cross_fma(d, e2);
+    float det = dot_fma(e1, pv);
     const unsigned sg = __float_as_uint(det) & 0x80000000u;
     const float adet = fabsf(det);
     f3 s = o - v0;
-    float u = __uint_as_float(__float_as_uint(dot(s, pv)) ^ sg);
-    f3 q = cross(s, e1);
-    float v = __uint_as_float(__float_as_uint(dot(d, q)) ^ sg);
-    float t = __uint_as_float(__float_as_uint(dot(e2, q)) ^ sg);
+    float u = __uint_as_float(__float_as_uint(dot_fma(s, pv)) ^ sg);
+    f3 q = cross_fma(s, e1);
+    float v = __uint_as_float(__float_as_uint(dot_fma(d, q)) ^ sg);
+    float t = __uint_as_float(__float_as_uint(dot_fma(e2, q)) ^ sg);
     // u <= |det| is implied by v >= 0 and RN(u + v) <= |det| (see mt_segs)
     return (u >= 0.0f) & (v >= 0.0f) & ((u + v) <= adet) & (t > tmin * adet) & (t < tmax * adet);
 }

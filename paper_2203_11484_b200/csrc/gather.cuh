@@ -99,20 +99,20 @@ __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, 
     const f3 v0 = xyz(a), e1 = xyz(b), e2 = xyz(c);
     const f3 s = o - v0;
     unsigned hit = 0;
-    const f3 q = cross(s, e1);
-    const float tq = dot(e2, q);
+    const f3 q = cross_fma(s, e1);
+    const float tq = dot_fma(e2, q);
 #pragma unroll
     for (int k = 0; k < kGroup; ++k) {
         if (mask & (1u << k)) {
             if (kCount) st->tris += 1;
             const f3 d = S.d[k];
-            const f3 pv = cross(d, e2);
-            const float det = dot(e1, pv);
+            const f3 pv = cross_fma(d, e2);
+            const float det = dot_fma(e1, pv);
             // O9 any hit, division-free (reading R25): sign-normalised by det (exact negations)
             const unsigned sg = __float_as_uint(det) & 0x80000000u;
             const float adet = fabsf(det);
-            const float u = __uint_as_float(__float_as_uint(dot(s, pv)) ^ sg);
-            const float v = __uint_as_float(__float_as_uint(dot(d, q)) ^ sg);
+            const float u = __uint_as_float(__float_as_uint(dot_fma(s, pv)) ^ sg);
+            const float v = __uint_as_float(__float_as_uint(dot_fma(d, q)) ^ sg);
             const float t = __uint_as_float(__float_as_uint(tq) ^ sg);
             // (det = +-0 or NaN: t > tmin*|det| and t < tmax*|det| cannot both hold.  O9's u <= |det|
             // is implied: v >= 0 makes RN(u + v) >= u, so RN(u + v) <= |det| gives u <= |det|; a NaN
