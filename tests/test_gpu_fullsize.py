@@ -7,6 +7,8 @@ indirect image and every pixel x VPL visibility bit on sampled pixels; C5
 labels, sampled walks, G-buffer samples and a VPL-subset gather."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -59,7 +61,9 @@ def test_full_frame_parity(cfg, n_px):
     for k in ("pos", "nrm", "alb", "t"):
         assert np.array_equal(g[k][hit].view(np.uint32), og[k][hit].view(np.uint32)), k
     # gather + visibility bits on sampled pixels (BJ:5 tolerances)
+    n_px *= int(os.environ.get("VPLGI_PARITY_SCALE", "1"))    # extended runs (profiles/r01_extended_parity.txt)
     c = _check_gather(r, o, sample_pixels(s.width, s.height, n_px, seed=100 + cfg))
+    print(f"C{cfg} {n_px} px: {c}")
     assert c["tmis"] == 0, c
     assert c["vmis"] <= VIS_TOL * max(c["ntr"], 1) + 1, c
     assert c["mre"] <= MRE_TOL and c["prel"] <= PIXEL_TOL, c
