@@ -29,9 +29,11 @@ def _headers():
 def build(force: bool = False, verbose: bool = False, defines: tuple = (), out: Path | None = None) -> Path:
     """Build libvplgi.so; `defines`/`out` build a tuning variant (tools/ only) into its own file."""
     lib = Path(out) if out else LIB
-    obj = OBJ if not defines else OBJ / ("v_" + "_".join(d.replace("=", "") for d in defines))
+    extra = os.environ.get("VPLGI_NVCC_EXTRA", "").split() if out else []   # tuning variants only (tools/)
+    tag = [d.replace("=", "") for d in defines] + [e.strip("-").replace("=", "") for e in extra]
+    obj = OBJ if not tag else OBJ / ("v_" + "_".join(tag))
     obj.mkdir(parents=True, exist_ok=True)
-    flags = NVCC_FLAGS + [f"-D{d}" for d in defines]
+    flags = NVCC_FLAGS + [f"-D{d}" for d in defines] + extra
     hdr_mtime = max(p.stat().st_mtime for p in _headers())
     objs = []
     for src in SOURCES:
