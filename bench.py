@@ -100,7 +100,7 @@ class ClockSampler:
 # segment setup, so those count as separate FMUL/FADD; the any-hit MT counts
 # the fused form of reading R26; square roots and divisions count as one MUFU
 # op each.  (fma, alu, mufu) per unit:
-OPS = {"pairs": (18, 3, 0),       # d (3), r^2 (5), cx (5), ci (5) | tri, cx, ci tests                 (O13)
+OPS = {"pairs": (14, 3, 0),       # d (3), r^2 (5), cx (3, fused), ci (3, fused) | tri, cx, ci tests (O13, R26)
        "traced": (9, 2, 2),       # tmax, cx*ci, r2*max, 3 FFMA, d*inv (3) | test, max | sqrt, 1/dist  (O9, O13, R25)
        "box_tests": (12, 5, 0),   # per-ray slab (centre/half-extent): 3 FFMA + 3 FMUL + 6 FADD | 4 min/max + cmp
        "cone_tests": (6, 11, 0),  # beam x child box: 6 FFMA | 6 SEL + 4 min/max + 1 cmp (gather.cuh beam_box)

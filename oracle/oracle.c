@@ -713,8 +713,9 @@ void oracle_gather(const OScene* s, const OGbuf* gb, int64_t n_pix, const OVpl* 
                 f3 y = ld3(v[i].pos);
                 f3 d = sub(y, x);
                 float r2 = dot(d, d);
-                float cx = dot(nx, d);
-                float ci = -dot(ld3(v[i].nrm), d);
+                f3 ni = ld3(v[i].nrm);               /* R26: the cosine terms as fused dots */
+                float cx = fmaf(nx.z, d.z, fmaf(nx.y, d.y, nx.x * d.x));
+                float ci = -fmaf(ni.z, d.z, fmaf(ni.y, d.y, ni.x * d.x));
                 if (!(cx > 0.0f && ci > 0.0f)) continue;
                 total_traced++;
                 if (traced_bits) traced_bits[k * words + i / 32] |= 1u << (i % 32);

@@ -372,8 +372,8 @@ __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_rec
             const int tri_i = yt[k];
             const f3 d = yk[k] - x;
             const float r2 = dot(d, d);
-            const float cx = dot(nx, d);
-            const float ci = -dot(xyz(nb), d);
+            const float cx = dot_fma(nx, d);          // R26: the cosine terms as fused dots
+            const float ci = -dot_fma(xyz(nb), d);
             if (active && tri_i != tri_x && cx > 0.0f && ci > 0.0f) {
                 traced |= 1u << k;
                 w[k] = __fdividef(cx * ci, r2 * fmaxf(r2, b2));
