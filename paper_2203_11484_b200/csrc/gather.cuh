@@ -8,8 +8,8 @@
 // receiver (exact fp32, O13), and the shadow segments x_j -> y that need a
 // visibility test are resolved together:
 //   1. occluder cache: exact MT tests against the lane's two latest occluders
-//      and the warp's latest one, skipped by lanes whose last traced segment
-//      was visible;
+//      (and, with VPL_CACHE_WARP, the warp's latest one), skipped by lanes
+//      whose last traced segment was visible;
 //   2. beam traversal of the 16-wide BVH (leaves = single triangles): all
 //      remaining segments lie in the beam {y + s*D : y in Ybox, D in Dbox,
 //      s in [s_lo, s_hi]}; lane c of each half-warp tests child c of a node
@@ -44,7 +44,7 @@ namespace vplgi {
 #define VPL_CACHE_OWN2 1    // test the lane's second most recent occluder
 #endif
 #ifndef VPL_CACHE_WARP
-#define VPL_CACHE_WARP 1    // test the warp's most recent occluder
+#define VPL_CACHE_WARP 0    // 1: also test the warp's most recent occluder (v20: +0.8% at C4, off)
 #endif
 #ifndef VPL_GROUP_TOL
 #define VPL_GROUP_TOL 0.05f
@@ -317,9 +317,13 @@ __device__ __forceinline__ void resolve_group(const BvhView& bv, f3 x, Segs& S, 
         }
     }
     S.pend = 0;
+#if VPL_CACHE_WARP
     // share the newest occluder found in this resolution with the whole warp
     const unsigned fresh = __ballot_sync(0xFFFFFFFFu, (S.occ & ~had) != 0);
     if (fresh) cache.warp = __shfl_sync(0xFFFFFFFFu, cache.own0, __ffs(fresh) - 1);
+#else
+    (void)had;
+#endif
 }
 
 // The VPL group starting at i (uniform): the longest run of <= kGroup VPLs in
