@@ -16,7 +16,7 @@
 namespace vplgi {
 
 #ifndef VPL_PLOC_RADIUS
-#define VPL_PLOC_RADIUS 64   // PLOC search radius: 64 gives a 3% faster gather at C4 than 16 (+1.2 ms build)
+#define VPL_PLOC_RADIUS 128  // PLOC search radius: vs 64, C4 gather -4.8%, C5 -10%, C3 +2% (+1.2 ms build)
 #endif
 constexpr int kPlocRadius = VPL_PLOC_RADIUS;
 constexpr int kPlocBlock = 256;

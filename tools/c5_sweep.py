@@ -2,6 +2,7 @@
 GPU, near fraction swept over 50/80/95% (BJ:11): one frame of a1-a8, the
 gather timed with CUDA events, counters from the counter build.  BJ runs C5
 across 8 GPUs; this pod has one, so these are the per-GPU numbers."""
+import os
 import json
 import sys
 from pathlib import Path
@@ -13,7 +14,7 @@ import torch  # noqa: E402
 import paper_2203_11484_b200 as V  # noqa: E402
 import scenegen  # noqa: E402
 
-for f in (0.5, 0.8, 0.95):
+for f in [float(x) for x in os.environ.get("VPLGI_C5_FRACS", "0.5,0.8,0.95").split(",")]:
     s = scenegen.make_scene(5, near_frac=f)
     r = V.Renderer(s)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
