@@ -16,6 +16,16 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 SRC = HERE / "oracle.c"
 LIB = HERE / "liboracle.so"
+LIB_O0 = HERE / "liboracle_o0.so"   # frozen O0 variant (-DORACLE_O0=1): SPEC S:134-150 MT, no fma
+VARIANTS = {"default": (LIB, []), "o0": (LIB_O0, ["-DORACLE_O0=1"])}
+_default_variant = "default"
+
+
+def set_default_variant(v: str) -> None:
+    """Variant OracleScene uses when none is given (tests parametrise the pins over both)."""
+    global _default_variant
+    assert v in VARIANTS, v
+    _default_variant = v
 
 CFLAGS = ["-O3", "-march=x86-64-v3", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
           "-fPIC", "-shared", "-std=c11", "-Wall", "-Wno-unused-function"]
@@ -43,21 +53,22 @@ class OInfo(C.Structure):
 
 
 def build(force: bool = False) -> Path:
-    if force or not LIB.exists() or LIB.stat().st_mtime < SRC.stat().st_mtime:
-        tmp = LIB.with_suffix(f".{os.getpid()}.tmp.so")
-        subprocess.check_call(["gcc", *CFLAGS, "-o", str(tmp), str(SRC), "-lm"])
-        os.replace(tmp, LIB)
+    for path, defs in VARIANTS.values():
+        if force or not path.exists() or path.stat().st_mtime < SRC.stat().st_mtime:
+            tmp = path.with_suffix(f".{os.getpid()}.tmp.so")
+            subprocess.check_call(["gcc", *CFLAGS, *defs, "-o", str(tmp), str(SRC), "-lm"])
+            os.replace(tmp, path)
     return LIB
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def lib(variant: str | None = None):
+    variant = variant or "default"
+    if variant not in _libs:
         build()
-        L = C.CDLL(str(LIB))
+        L = C.CDLL(str(VARIANTS[variant][0]))
         P, I64, F, U8, U32, U64 = C.c_void_p, C.c_int64, C.c_float, C.c_uint8, C.c_uint32, C.c_uint64
         sig = {
             "oracle_philox4x32_10": (None, [P, P, P]),
@@ -89,14 +100,16 @@ def lib():
             "oracle_near_strata": (I64, [P, P, P, I64, I64, I64, P]),
             "oracle_walk_range": (None, [P, P, P, I64, I64, P, P]),
             "oracle_abi": (C.c_int, []),
+            "oracle_variant": (C.c_int, []),
             "oracle_threads": (C.c_int, []),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        _lib = L
-    return _lib
+        assert L.oracle_variant() == (variant == "o0")
+        _libs[variant] = L
+    return _libs[variant]
 
 
 def _p(a: np.ndarray):
@@ -135,7 +148,9 @@ def threads() -> int:
 class OracleScene:
     """Oracle view of a scenegen.Scene (or raw arrays)."""
 
-    def __init__(self, scene):
+    def __init__(self, scene, variant: str | None = None):
+        self.variant = variant or _default_variant
+        self.L = lib(self.variant)
         self.scene = scene
         self._keep = [np.ascontiguousarray(scene.verts, np.float32),
                       np.ascontiguousarray(scene.albedo, np.float32),
@@ -143,56 +158,56 @@ class OracleScene:
                       np.ascontiguousarray(scene.cam, np.float32)]
         V, A, Lt, Cm = self._keep
         self.n = V.shape[0]
-        self.h = lib().oracle_scene_new(_p(V), _p(A), self.n, _p(Lt), Lt.shape[0], _p(Cm),
+        self.h = self.L.oracle_scene_new(_p(V), _p(A), self.n, _p(Lt), Lt.shape[0], _p(Cm),
                                         scene.width, scene.height)
         if not self.h:
             raise ValueError("oracle_scene_new failed")
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().oracle_scene_free(self.h)
+            self.L.oracle_scene_free(self.h)
             self.h = None
 
     # ---- O1 ----
     @property
     def bad(self) -> int:
-        return int(lib().oracle_scene_bad(self.h))
+        return int(self.L.oracle_scene_bad(self.h))
 
     def consts(self):
         d, e, b = C.c_double(), C.c_float(), C.c_float()
-        lib().oracle_scene_consts(self.h, C.byref(d), C.byref(e), C.byref(b))
+        self.L.oracle_scene_consts(self.h, C.byref(d), C.byref(e), C.byref(b))
         return d.value, np.float32(e.value), np.float32(b.value)
 
     def tri_data(self):
         n = self.n
         nrm, cen = np.zeros((n, 3), np.float32), np.zeros((n, 3), np.float32)
         area, aq = np.zeros(n, np.float32), np.zeros(n, np.uint64)
-        lib().oracle_tri_data(self.h, _p(nrm), _p(cen), _p(area), _p(aq))
+        self.L.oracle_tri_data(self.h, _p(nrm), _p(cen), _p(area), _p(aq))
         return dict(normal=nrm, centroid=cen, area=area, aq=aq)
 
     # ---- O9 ----
     def closest_hit(self, o, d, tmin=0.0, tmax=np.inf):
         o = np.asarray(o, np.float32); d = np.asarray(d, np.float32)
         t = C.c_float()
-        i = lib().oracle_closest_hit(self.h, _p(o), _p(d), tmin, tmax, C.byref(t))
+        i = self.L.oracle_closest_hit(self.h, _p(o), _p(d), tmin, tmax, C.byref(t))
         return int(i), np.float32(t.value)
 
     def closest_batch(self, o, d, tmin=0.0, tmax=np.inf):
         o = np.ascontiguousarray(o, np.float32).reshape(-1, 3)
         d = np.ascontiguousarray(d, np.float32).reshape(-1, 3)
         idx, t = np.zeros(len(o), np.int64), np.zeros(len(o), np.float32)
-        lib().oracle_closest_batch(self.h, _p(o), _p(d), len(o), tmin, tmax, _p(idx), _p(t))
+        self.L.oracle_closest_batch(self.h, _p(o), _p(d), len(o), tmin, tmax, _p(idx), _p(t))
         return idx, t
 
     def occluded(self, a, b) -> bool:
         a = np.asarray(a, np.float32); b = np.asarray(b, np.float32)
-        return bool(lib().oracle_occluded(self.h, _p(a), _p(b)))
+        return bool(self.L.oracle_occluded(self.h, _p(a), _p(b)))
 
     def occluded_batch(self, a, b):
         a = np.ascontiguousarray(a, np.float32).reshape(-1, 3)
         b = np.ascontiguousarray(b, np.float32).reshape(-1, 3)
         out = np.zeros(len(a), np.uint8)
-        lib().oracle_occluded_batch(self.h, _p(a), _p(b), len(a), _p(out))
+        self.L.oracle_occluded_batch(self.h, _p(a), _p(b), len(a), _p(out))
         return out.astype(bool)
 
     # ---- O2 ----
@@ -200,26 +215,26 @@ class OracleScene:
         T = self.scene.T if T is None else T
         labels = np.zeros(self.n, np.uint8)
         nn = C.c_int64()
-        lib().oracle_classify(self.h, float(T), _p(labels), C.byref(nn))
+        self.L.oracle_classify(self.h, float(T), _p(labels), C.byref(nn))
         return labels, int(nn.value)
 
     # ---- O3-O5 ----
     def lit(self, labels):
         labels = np.ascontiguousarray(labels, np.uint8)
         out = np.zeros(self.n, np.uint8)
-        lib().oracle_lit(self.h, _p(labels), _p(out))
+        self.L.oracle_lit(self.h, _p(labels), _p(out))
         return out
 
     def near_table(self, lit):
         lit = np.ascontiguousarray(lit, np.uint8)
         order, P = np.zeros(self.n, np.int64), np.zeros(self.n, np.uint64)
         codes = np.zeros(self.n, np.uint32)
-        m = lib().oracle_near_table(self.h, _p(lit), _p(order), _p(P), _p(codes))
+        m = self.L.oracle_near_table(self.h, _p(lit), _p(order), _p(P), _p(codes))
         return order[:m], P[:m], codes[:m]
 
     def point_in_tri(self, t, u1, u2):
         out = np.zeros(3, np.float32)
-        lib().oracle_point_in_tri(self.h, int(t), float(u1), float(u2), _p(out))
+        self.L.oracle_point_in_tri(self.h, int(t), float(u1), float(u2), _p(out))
         return out
 
     # ---- O3-O11 ----
@@ -234,7 +249,7 @@ class OracleScene:
         out = np.zeros(cap, VPL_DTYPE)
         info = OInfo()
         labels = np.ascontiguousarray(labels, np.uint8)
-        n = lib().oracle_generate_vpls(self.h, _p(labels), C.byref(p), _p(out), cap, C.byref(info))
+        n = self.L.oracle_generate_vpls(self.h, _p(labels), C.byref(p), _p(out), cap, C.byref(info))
         if n < 0:
             raise RuntimeError("oracle_generate_vpls: output capacity too small")
         return out[:n].copy(), info.as_dict()
@@ -250,7 +265,7 @@ class OracleScene:
         p = self._params(**kw)
         out = np.zeros(max(k1 - k0, 0), VPL_DTYPE)
         labels = np.ascontiguousarray(labels, np.uint8)
-        lib().oracle_near_strata(self.h, _p(labels), C.byref(p), K, k0, k1, _p(out))
+        self.L.oracle_near_strata(self.h, _p(labels), C.byref(p), K, k0, k1, _p(out))
         return out
 
     def walk_range(self, labels, w0, w1, **kw):
@@ -260,14 +275,14 @@ class OracleScene:
         dep = np.zeros((w1 - w0) * md, VPL_DTYPE)
         cnt = np.zeros(w1 - w0, np.int32)
         labels = np.ascontiguousarray(labels, np.uint8)
-        lib().oracle_walk_range(self.h, _p(labels), C.byref(p), w0, w1, _p(dep), _p(cnt))
+        self.L.oracle_walk_range(self.h, _p(labels), C.byref(p), w0, w1, _p(dep), _p(cnt))
         return np.concatenate([dep[i * md:i * md + c] for i, c in enumerate(cnt)]) if len(cnt) else dep[:0]
 
     # ---- O12 ----
     def gbuffer(self, pixels):
         pixels = np.ascontiguousarray(pixels, np.int32)
         out = np.zeros(len(pixels), GBUF_DTYPE)
-        lib().oracle_gbuffer(self.h, _p(pixels), len(pixels), _p(out))
+        self.L.oracle_gbuffer(self.h, _p(pixels), len(pixels), _p(out))
         return out
 
     # ---- O13 ----
@@ -281,7 +296,7 @@ class OracleScene:
         words = (M + 31) // 32
         tb = np.zeros((n, words), np.uint32) if bits else None
         vb = np.zeros((n, words), np.uint32) if bits else None
-        lib().oracle_gather(self.h, _p(gb), n, _p(vpls), M, _p(rgb), _p(rgb64), C.byref(traced),
+        self.L.oracle_gather(self.h, _p(gb), n, _p(vpls), M, _p(rgb), _p(rgb64), C.byref(traced),
                             _p(tb) if bits else None, _p(vb) if bits else None)
         res = dict(rgb=rgb, rgb64=rgb64, traced=int(traced.value))
         if bits:
@@ -296,7 +311,7 @@ class OracleScene:
         pixels = np.ascontiguousarray(pixels, np.int32)
         rgb = np.zeros((len(gb), 3), np.float32)
         seed = self.scene.seed if seed is None else seed
-        lib().oracle_direct(self.h, _p(gb), _p(pixels), len(gb), int(S), int(seed), float(np.float32(1.0 / S)),
+        self.L.oracle_direct(self.h, _p(gb), _p(pixels), len(gb), int(S), int(seed), float(np.float32(1.0 / S)),
                             _p(rgb))
         return rgb
 
@@ -304,7 +319,7 @@ class OracleScene:
     def probe_pixels(self, seed=None):
         out = np.zeros(64, np.int32)
         s = self.scene
-        lib().oracle_probe_pixels(s.width, s.height, int(s.seed if seed is None else seed), _p(out))
+        self.L.oracle_probe_pixels(s.width, s.height, int(s.seed if seed is None else seed), _p(out))
         return out
 
     def rejection(self, pilot, budget, seed=None, gb=None):
@@ -325,7 +340,7 @@ class OracleScene:
         sc = np.zeros(max(len(pilot), 1), np.float32)
         mean = C.c_double()
         scanned = C.c_int64()
-        acc = lib().oracle_rejection(self.h, _p(gb), len(gb), _p(pilot), len(pilot), int(budget), int(seed), _p(out),
+        acc = self.L.oracle_rejection(self.h, _p(gb), len(gb), _p(pilot), len(pilot), int(budget), int(seed), _p(out),
                                      _p(sc), C.byref(mean), C.byref(scanned))
         return out[:acc], dict(accepted=int(acc), mean=float(mean.value), scores=sc[:len(pilot)],
                                n_scanned=int(scanned.value), probes=px)
@@ -344,7 +359,7 @@ class OracleScene:
         sc = np.zeros(len(pilot), np.float32)
         pool = np.zeros(len(pilot), np.int64)
         acc = C.c_int64()
-        lib().oracle_metropolis(self.h, _p(gb), len(gb), _p(pilot), len(pilot), int(chains), int(per_chain),
+        self.L.oracle_metropolis(self.h, _p(gb), len(gb), _p(pilot), len(pilot), int(chains), int(per_chain),
                                 int(burn), int(radius), int(seed), _p(out), _p(sc), _p(pool), C.byref(acc))
         return out[:n], dict(scores=sc, pool=pool, accepted=int(acc.value))
 
@@ -352,5 +367,5 @@ class OracleScene:
         x = np.ascontiguousarray(x, np.float32).reshape(-1, 3)
         y = np.ascontiguousarray(y, np.float32).reshape(-1, 3)
         out = np.zeros(len(x), np.uint8)
-        lib().oracle_pair_visibility(self.h, _p(x), _p(y), len(x), _p(out))
+        self.L.oracle_pair_visibility(self.h, _p(x), _p(y), len(x), _p(out))
         return out.astype(bool)

@@ -27,6 +27,15 @@
 #endif
 
 #define ORACLE_ABI 1
+/* ORACLE_O0 = 1 builds the frozen O0 variant (liboracle_o0.so): SURVEY      */
+/* §8(c) O0/O9 exactly as SPEC S:134-150 writes Moller-Trumbore — no fused  */
+/* multiply-add anywhere, inv = 1/det for the any hit too, dir = d/dist     */
+/* componentwise, and O13's cosine terms as plain dots.  The default build  */
+/* keeps readings R25/R26.  Both are the same real-number    */
+/* predicates; tests compare the CUDA path with both within BJ:5's budget.  */
+#ifndef ORACLE_O0
+#define ORACLE_O0 0
+#endif
 #define PI_D 3.14159265358979323846 /* pi, rounded once to double */
 
 typedef struct { float x, y, z; } f3;
@@ -191,6 +200,25 @@ void oracle_tri_data(const OScene* s, float* nrm, float* cen, float* area, uint6
 /* ------------------------------------------------------------------------ */
 #define CHUNK 2048
 
+#if ORACLE_O0
+/* O0 any hit: SPEC S:134-150 verbatim (inv = 1/det, no fma) */
+static int any_hit_chunk(const OScene* s, f3 o, f3 d, float tmin, float tmax, int64_t i0, int64_t i1) {
+    int hit = 0;
+    for (int64_t i = i0; i < i1; i++) {
+        f3 e1 = mk(s->e1x[i], s->e1y[i], s->e1z[i]), e2 = mk(s->e2x[i], s->e2y[i], s->e2z[i]);
+        f3 pv = cross(d, e2);
+        float det = dot(e1, pv);
+        float inv = 1.0f / det;
+        f3 sv = sub(o, mk(s->v0x[i], s->v0y[i], s->v0z[i]));
+        float u = dot(sv, pv) * inv;
+        f3 q = cross(sv, e1);
+        float v = dot(d, q) * inv;
+        float t = dot(e2, q) * inv;
+        hit |= (det != 0.0f) & (u >= 0.0f) & (u <= 1.0f) & (v >= 0.0f) & ((u + v) <= 1.0f) & (t > tmin) & (t < tmax);
+    }
+    return hit;
+}
+#else
 static int any_hit_chunk(const OScene* s, f3 o, f3 d, float tmin, float tmax, int64_t i0, int64_t i1) {
     int hit = 0;
     for (int64_t i = i0; i < i1; i++) {
@@ -215,6 +243,7 @@ static int any_hit_chunk(const OScene* s, f3 o, f3 d, float tmin, float tmax, in
     }
     return hit;
 }
+#endif
 
 static int any_hit(const OScene* s, f3 o, f3 d, float tmin, float tmax) {
     for (int64_t i0 = 0; i0 < s->n; i0 += CHUNK) {
@@ -276,8 +305,12 @@ static int64_t closest_hit(const OScene* s, f3 o, f3 d, float tmin, float tmax, 
 static int occluded(const OScene* s, f3 a, f3 b) {
     f3 d = sub(b, a);
     float dist = sqrtf(dot(d, d));
+#if ORACLE_O0
+    f3 dir = mk(d.x / dist, d.y / dist, d.z / dist);   /* O9: dir = d / dist */
+#else
     float inv = 1.0f / dist;                       /* R25: one division, three products */
     f3 dir = mk(d.x * inv, d.y * inv, d.z * inv);
+#endif
     float tmin = s->eps, tmax = dist - s->eps;
     if (!(tmax > tmin)) return 0;
     return any_hit(s, a, dir, tmin, tmax);
@@ -714,8 +747,13 @@ void oracle_gather(const OScene* s, const OGbuf* gb, int64_t n_pix, const OVpl* 
                 f3 d = sub(y, x);
                 float r2 = dot(d, d);
                 f3 ni = ld3(v[i].nrm);               /* R26: the cosine terms as fused dots */
+#if ORACLE_O0
+                float cx = dot(nx, d);                /* O13 as written: plain dots */
+                float ci = -dot(ni, d);
+#else
                 float cx = fmaf(nx.z, d.z, fmaf(nx.y, d.y, nx.x * d.x));
                 float ci = -fmaf(ni.z, d.z, fmaf(ni.y, d.y, ni.x * d.x));
+#endif
                 if (!(cx > 0.0f && ci > 0.0f)) continue;
                 total_traced++;
                 if (traced_bits) traced_bits[k * words + i / 32] |= 1u << (i % 32);
@@ -1001,6 +1039,7 @@ void oracle_walk_range(const OScene* s, const uint8_t* labels, const OParams* p,
 }
 
 int oracle_abi(void) { return ORACLE_ABI; }
+int oracle_variant(void) { return ORACLE_O0; }   /* 1: the frozen O0 build */
 int oracle_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

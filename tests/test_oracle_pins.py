@@ -20,6 +20,15 @@ HERE = Path(__file__).resolve().parent
 INV_PI32 = np.float32(1.0 / math.pi)
 
 
+@pytest.fixture(autouse=True, params=["default", "o0"])
+def oracle_variant(request):
+    """Every pin runs against both oracle builds: the default one (readings
+    R25/R26) and the frozen O0 one (SPEC S:134-150 MT, no fma)."""
+    oracle.set_default_variant(request.param)
+    yield request.param
+    oracle.set_default_variant("default")
+
+
 # ---------------------------------------------------------------- helpers
 def F_c(X, Y):
     """Point-to-parallel-rectangle form factor for a point under the corner of
@@ -339,6 +348,42 @@ def test_eq2_fully_occluded_light_gives_zero_flux():
     lab2, _ = o2.classify()
     v2, info2 = o2.generate_vpls(lab2)
     assert info2["K"] == 64 and np.all(v2["flux"] > 0)
+
+
+def test_lit_uses_the_light_centre_point():
+    """R6 ("visible to the light source"): the lit test is the
+    centroid -> light-centre segment.  Hand geometry: a 4 cm blocker on that
+    segment (1 m up) leaves every light-corner segment free, so a corner-point
+    test would call the patch lit; a blocker on one corner segment only must
+    leave it lit."""
+    h = 1e-2
+    recv = [[-h, 0, -h], [-h, 0, h], [h, 0, -h]]            # normal +y, centroid (-h/3, 0, -h/3)
+    cam = scenegen.make_camera([0.0, 0.5, -0.5], [0, 0, 0], 60.0, 8, 8)
+
+    def lit_of(blocker_centre):
+        b = np.asarray(blocker_centre, np.float64) + [0.005, 0.0, -0.003]   # segment off the quad's diagonal
+        V = [recv, *scenegen.quad_tris(b + [-0.02, 0, -0.02], [0.04, 0, 0], [0, 0, 0.04])]
+        o = oracle.OracleScene(tiny_scene(V, cam=cam, T=5.0, M=64, K_near=64, seed=1))
+        lab, _ = o.classify()
+        assert lab[0] == 1
+        return int(o.lit(lab)[0]), o
+
+    c = np.array([-h / 3, 0.0, -h / 3])
+    Lc = np.array([0.0, 1.999, 0.0])
+    corners = [Lc + [sx * 0.25, 0, sz * 0.25] for sx in (-1, 1) for sz in (-1, 1)]
+    # blocker on the centre segment: no corner segment meets it (float64 geometry), yet unlit
+    at = c + (Lc - c) * (1.0 / 1.999)
+    lit, o = lit_of(at)
+    for q in corners:
+        assert o.occluded(c.astype(np.float32), q.astype(np.float32)) is False
+    assert o.occluded(c.astype(np.float32), Lc.astype(np.float32)) is True
+    assert lit == 0
+    # blocker on the (+x, +z) corner segment only: the centre segment is free, so lit
+    q = corners[3]
+    lit, o = lit_of(c + (q - c) * (1.0 / 1.999))
+    assert o.occluded(c.astype(np.float32), q.astype(np.float32)) is True
+    assert o.occluded(c.astype(np.float32), Lc.astype(np.float32)) is False
+    assert lit == 1
 
 
 def test_near_vpls_represent_equal_area_and_sit_on_lit_triangles():
