@@ -42,7 +42,7 @@ extern "C" {
 #define VPL_API
 #endif
 
-#define VPL_ABI_VERSION 2   /* 2: vpl_gather_bytes(M, W, H), vpl_counters.cache_tests, f1-f4 entry points */
+#define VPL_ABI_VERSION 3   /* 3: vpl_counters.cand_*, filter_steps; 2: vpl_gather_bytes(M, W, H), vpl_counters.cache_tests, f1-f4 entry points */
 #define VPL_MAX_LIGHTS 64
 
 enum {
@@ -128,6 +128,11 @@ typedef struct {
     unsigned long long ray_packets;  /* packets traversed with per-ray tests (loose cones) */
     unsigned long long cache_hits;   /* traced lanes resolved by the occluder cache */
     unsigned long long cache_tests;  /* exact MT tests spent in the occluder cache (part of tri_tests) */
+    unsigned long long cand_lists;   /* VPL clusters whose candidate-triangle list was built */
+    unsigned long long cand_entries; /* total entries of those lists */
+    unsigned long long cand_fails;   /* clusters whose list could not be used (loose beam or overflow) */
+    unsigned long long filter_steps; /* per-VPL candidate-filter iterations (32 candidates each) */
+    unsigned long long cand_steps;   /* traversal steps spent building the lists (part of warp_steps) */
 } vpl_counters;
 
 /* -------------------------------------------------------------------- */

@@ -52,7 +52,8 @@ class vpl_gen_info(C.Structure):
 
 
 COUNTER_NAMES = ["pairs", "traced", "visible", "box_tests", "tri_tests", "warp_rays", "warp_steps", "cone_tests",
-                 "cone_packets", "ray_packets", "cache_hits", "cache_tests"]
+                 "cone_packets", "ray_packets", "cache_hits", "cache_tests", "cand_lists", "cand_entries", "cand_fails",
+                 "filter_steps", "cand_steps"]
 
 
 class vpl_counters(C.Structure):
@@ -60,7 +61,7 @@ class vpl_counters(C.Structure):
 
 
 def counters_dict(ctr) -> dict:
-    """vpl_counters tensor (int64[11]) -> {name: int}"""
+    """vpl_counters tensor (int64[len(COUNTER_NAMES)]) -> {name: int}"""
     vals = ctr.tolist() if hasattr(ctr, "tolist") else list(ctr)
     return {k: int(v) for k, v in zip(COUNTER_NAMES, vals)}
 

@@ -305,6 +305,9 @@ struct TravStats {
     uint32_t wrays = 0, wsteps = 0;  // warp-level packets / iterations (counted on lane 0)
     uint32_t cones = 0, cpk = 0, rpk = 0, chits = 0;  // cone tests, cone / per-ray packets, cache hits
     uint32_t ctests = 0;                              // MT tests in the occluder cache
+    uint32_t lists = 0, entries = 0, lfail = 0;       // cluster candidate lists built / their entries / unusable
+    uint32_t fsteps = 0;                              // candidate-filter iterations (32 candidates each)
+    uint32_t lsteps = 0;                              // traversal steps spent building candidate lists
 };
 
 // leaf refs: ~((first << 3) | (count - 1)), count in [1, 8]

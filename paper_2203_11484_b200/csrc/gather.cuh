@@ -49,6 +49,21 @@ namespace vplgi {
 #ifndef VPL_GROUP_TOL
 #define VPL_GROUP_TOL 0.05f
 #endif
+#ifndef VPL_CANDS
+#define VPL_CANDS 1         // per-cluster candidate-triangle lists (one beam traversal per 32-VPL cluster)
+#endif
+#ifndef VPL_CAND_CAP
+#define VPL_CAND_CAP 128    // list capacity (entries at the top of the warp's stack array); C4: 64 / 128 / 192 / 256 measured, 128 best
+#endif
+#ifndef VPL_CAND_GROUP
+#define VPL_CAND_GROUP 16     // a list covers the next VPL_CAND_GROUP VPLs of the cluster from the first that needs it
+                              // (C4: 8 / 12 / 16 / 24 / 32 measured, 16 best)
+#endif
+#ifndef VPL_CAND_STRADDLE
+#define VPL_CAND_STRADDLE 1   // 1: also build lists for beams with straddling axes (extent test; C4 -3%)
+#endif
+constexpr int kCandCap = VPL_CAND_CAP;
+static_assert(kCandCap + 64 <= kWarpStack, "candidate list must leave room for the traversal stack");
 constexpr int kGroup = VPL_GROUP;          // max VPLs per group
 constexpr float kGroupTol = VPL_GROUP_TOL; // group iff the VPL box extent < tol * distance to the warp's receivers
 
@@ -59,9 +74,17 @@ constexpr float kGroupTol = VPL_GROUP_TOL; // group iff the VPL box extent < tol
 // actual segments).  Stored as s0 = N*a0 - b0, s1 = F*a1 - b1 with N/F the
 // box face picked by the sign of D_a; evaluated with one FFMA each.  The
 // rounding (position error ~ulp(coord)) is absorbed by the box padding.
+// beam bounds only (conservative by the box padding, never an O9 operand): one MUFU op each, with
+// flush-to-zero (a sub-normal component of D is ~0 against the padding; the plain .approx forms
+// expand to ~8 range-scaling instructions)
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
-    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
 
@@ -70,6 +93,9 @@ struct Beam {
     float s_lo, s_hi;
     unsigned pos;   // bit a: D_a > 0
 };
+
+__device__ __forceinline__ bool beam_from_bounds(const float* Dn, const float* Dm, const float* yl, const float* yh,
+                                                 float lmin, float lmax, float spread_tol, float eps, Beam& B);
 
 __device__ __forceinline__ bool beam_box(const Beam& B, float4 lo, float4 hi) {
     const bool px = B.pos & 1u, py = B.pos & 2u, pz = B.pos & 4u;
@@ -168,10 +194,17 @@ __device__ __forceinline__ bool make_beam(f3 x, const f3* yk, unsigned want, uns
         Dn[a] = warp_min_f32(dn[a]);
         Dm[a] = warp_max_f32(dm[a]);
     }
-    const float lmin = sqrtf(warp_min_f32(l2n));
-    const float lmax = sqrtf(warp_max_f32(l2m));
+    const float lmin = sqrt_approx(warp_min_f32(l2n));
+    const float lmax = sqrt_approx(warp_max_f32(l2m));
+    return beam_from_bounds(Dn, Dm, yl, yh, lmin, lmax, kConeSpread, eps, B);
+}
+
+// Beam {y + s*D : y in [yl, yh], D in [Dn, Dm], s in [s_lo, s_hi]} from uniform bounds; lmin / lmax
+// bound the segment lengths from below / above.  Returns false if the beam is loose.
+__device__ __forceinline__ bool beam_from_bounds(const float* Dn, const float* Dm, const float* yl, const float* yh,
+                                                 float lmin, float lmax, float spread_tol, float eps, Beam& B) {
     const float spread = fmax3(Dm[0] - Dn[0], Dm[1] - Dn[1], Dm[2] - Dn[2]);
-    bool tight = spread < kConeSpread * lmin;
+    bool tight = spread < spread_tol * lmin;
     B.pos = 0;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -188,9 +221,55 @@ __device__ __forceinline__ bool make_beam(f3 x, const f3* yk, unsigned want, uns
     }
     // segment (x_j, y_k) tests t in (eps, L - eps): s = 1 - t/L in (eps/L, 1 - eps/L) within
     // [eps/Lmax, 1 - eps/Lmax]; half the cap is cut (the rest is slack for MT's rounding of t)
-    B.s_lo = 0.5f * eps / lmax;
+    B.s_lo = (0.5f * eps) * rcp_approx(lmax);   // relative error ~1e-6: far inside the factor 1/2
     B.s_hi = 1.0f - B.s_lo;
     return tight;
+}
+
+// Beam of a whole VPL cluster: every segment from a participating receiver x_j to any point of the
+// cluster's position box [ylo, yhi] (a superset of the segments to the cluster's VPLs).  An axis on
+// which D changes sign ("straddling": the cluster and the receivers overlap along it) gives no
+// s-interval; its slab factor is made neutral (a0 = 0, b0 = +inf -> s0 = -inf; likewise s1 = +inf)
+// and replaced by the extent test lo <= U, hi >= L with [L, U] = [yl + Dn, yh + Dm] the range of the
+// segment points on that axis (s in [0, 1]).  Returns false only if every axis straddles.
+struct ClusterBeam {
+    Beam B;
+    float L[3], U[3];
+};
+__device__ __forceinline__ bool make_cluster_beam(f3 x, bool part, float4 ylo, float4 yhi, float eps, ClusterBeam& C) {
+    const float inf = __int_as_float(0x7f800000);
+    const float yl[3] = {ylo.x, ylo.y, ylo.z}, yh[3] = {yhi.x, yhi.y, yhi.z};
+    float Dn[3], Dm[3];
+    Dn[0] = warp_min_f32(part ? x.x - yhi.x : inf); Dm[0] = warp_max_f32(part ? x.x - ylo.x : -inf);
+    Dn[1] = warp_min_f32(part ? x.y - yhi.y : inf); Dm[1] = warp_max_f32(part ? x.y - ylo.y : -inf);
+    Dn[2] = warp_min_f32(part ? x.z - yhi.z : inf); Dm[2] = warp_max_f32(part ? x.z - ylo.z : -inf);
+    float l2n = 0.0f, l2m = 0.0f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {   // |D| over the box: per axis the nearer / farther face
+        const float n2 = Dn[a] * Dn[a], m2 = Dm[a] * Dm[a];
+        l2n += Dn[a] > 0.0f ? n2 : (Dm[a] < 0.0f ? m2 : 0.0f);
+        l2m += fmaxf(n2, m2);
+    }
+    beam_from_bounds(Dn, Dm, yl, yh, sqrt_approx(l2n), sqrt_approx(l2m), inf, eps, C.B);
+    int straddle = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const bool sa = !(Dn[a] > 0.0f) && !(Dm[a] < 0.0f);
+        C.L[a] = sa ? yl[a] + Dn[a] : -inf;
+        C.U[a] = sa ? yh[a] + Dm[a] : inf;
+        if (sa) {
+            ++straddle;
+            C.B.pos |= 1u << a;   // N = lo, F = hi
+            C.B.a0[a] = 0.0f; C.B.b0[a] = inf;
+            C.B.a1[a] = 0.0f; C.B.b1[a] = -inf;
+        }
+    }
+    return VPL_CAND_STRADDLE ? straddle < 3 : straddle == 0;
+}
+__device__ __forceinline__ bool cluster_beam_box(const ClusterBeam& C, float4 lo, float4 hi) {
+    const bool ext = (lo.x <= C.U[0]) & (lo.y <= C.U[1]) & (lo.z <= C.U[2]) & (hi.x >= C.L[0]) &
+                     (hi.y >= C.L[1]) & (hi.z >= C.L[2]);
+    return ext & beam_box(C.B, lo, hi);
 }
 
 // beam traversal (two nodes per step); returns when every lane's S.pend is 0 or the tree is exhausted
@@ -275,11 +354,133 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
     }
 }
 
+// Candidate list of a VPL cluster: one beam traversal of the 16-wide BVH with
+// the cluster beam (make_cluster_beam) that records every triangle child whose
+// box the beam reaches — no MT tests, no early exit.  Any triangle that can
+// block a segment of the cluster is in the list (the same conservative beam /
+// padded box argument as beam_traverse), so each VPL of the cluster then tests
+// only the list (filter_cands) instead of traversing the tree.  The list holds
+// 16-wide child slots (node * 16 + child) at the top of the warp's stack
+// array, in the order the traversal met them; returns its length, or -1 if
+// the beam is loose, the list overflows kCandCap or the stack meets the list.
+template <bool kCount>
+#ifndef VPL_CAND_NOINLINE
+#define VPL_CAND_NOINLINE 1   // keep the (rare) list build out of the hot loop's register allocation
+#endif
+#if VPL_CAND_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+int build_cands(const BvhView& bv, f3 x, bool part, const vpl_record* __restrict__ vg, int ng, float eps,
+                                        int* __restrict__ sstack, TravStats* st) {
+    const int lane = threadIdx.x & 31;
+    if (bv.root < 0) return -1;
+    // position box of the ng VPLs vg[0..ng) (lane l loads VPL l)
+    const float inf = __int_as_float(0x7f800000);
+    float4 ylo = make_float4(inf, inf, inf, 0.0f), yhi = make_float4(-inf, -inf, -inf, 0.0f);
+    if (lane < ng) { const float4 p = __ldg((const float4*)(vg + lane)); ylo = p; yhi = p; }
+    ylo.x = warp_min_f32(ylo.x); ylo.y = warp_min_f32(ylo.y); ylo.z = warp_min_f32(ylo.z);
+    yhi.x = warp_max_f32(yhi.x); yhi.y = warp_max_f32(yhi.y); yhi.z = warp_max_f32(yhi.z);
+    ClusterBeam CB;
+    if (!make_cluster_beam(x, part, ylo, yhi, eps, CB)) return -1;
+    const int half = lane >> 4;
+    const unsigned below = (1u << lane) - 1u;
+    const unsigned hmask = half ? 0xFFFF0000u : 0x0000FFFFu;
+    const unsigned dir_neg = CB.B.pos;
+    if (lane == 0) sstack[0] = bv.root;
+    __syncwarp();
+    int sp = 1, n = 0;
+    while (sp > 0) {
+        const int idx = sp - 1 - half;
+        const int node = idx >= 0 ? sstack[idx] : -1;
+        if (kCount && lane == 0) { st->wsteps += 1; st->lsteps += 1; }
+        sp = max(sp - 2, 0);
+        const int nsafe = node >= 0 ? node : 0;
+        const int slot = (nsafe << 4) + (lane & (kWide - 1));
+        const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)slot << 5));
+        const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
+        const int ref = node >= 0 ? __float_as_int(lo.w) : INT_MIN;
+        const int axis = __float_as_int(hi.w);
+        const bool hit = (ref != INT_MIN) & cluster_beam_box(CB, lo, hi);
+        if (kCount) {
+            const unsigned real = __ballot_sync(0xFFFFFFFFu, ref != INT_MIN);
+            if (lane == 0) st->cones += __popc(real);
+        }
+        const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
+        const unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
+        __syncwarp();
+        if (Bl) {
+            const int nl = __popc(Bl);
+            if (n + nl > kCandCap) {
+#ifdef VPL_CAND_DIAG
+                if (kCount && lane == 0) st->boxes += 1u << 20;   // diagnostic builds: overflow count in box_tests
+#endif
+                return -1;
+            }
+            if (hit && ref < 0) sstack[kWarpStack - 1 - (n + __popc(Bl & below))] = slot;
+            n += nl;
+        }
+        if (Bi) {
+            const int nB = __popc(Bi >> 16), nA = __popc(Bi & 0xFFFFu);
+            if (sp + nA + nB > kWarpStack - kCandCap) {
+#ifdef VPL_CAND_DIAG
+                if (kCount && lane == 0) st->boxes += 1u << 20;
+#endif
+                return -1;
+            }
+            const int rank = __popc(Bi & below & hmask);
+            const int nh = half ? nB : nA;
+            const bool rev = (dir_neg >> axis) & 1u;
+            const int pos = (half ? 0 : nB) + (rev ? rank : nh - 1 - rank);
+            if (hit && ref >= 0) sstack[sp + pos] = ref;
+            sp += nA + nB;
+        }
+        __syncwarp();
+    }
+    return n;
+}
+
+// The pending segments of one VPL against its cluster's candidate list: lane c
+// tests candidate c of each batch of 32 against the VPL's own beam; hit
+// triangles get the exact MT of O9 from every lane with a pending segment.
+template <bool kCount>
+__device__ __forceinline__ void filter_cands(const BvhView& bv, f3 x, Segs& S, float tmin, const Beam& B,
+                                             const int* __restrict__ sstack, int ncand, OccluderCache& cache,
+                                             TravStats* st) {
+    const int lane = threadIdx.x & 31;
+    for (int base = 0; base < ncand; base += 32) {
+        const int i = base + lane;
+        const bool ok = i < ncand;
+        const int slot = ok ? sstack[kWarpStack - 1 - i] : 0;   // slot 0: a real child, masked below
+        const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)slot << 5));
+        const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
+        const bool hit = ok & beam_box(B, lo, hi);
+        if (kCount && lane == 0) { st->fsteps += 1; st->cones += min(32, ncand - base); }
+        unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit);
+        const int ref = __float_as_int(lo.w);
+        while (Bl) {
+            const int k = __ffs(Bl) - 1;
+            Bl &= Bl - 1u;
+            const int tri = ~__shfl_sync(0xFFFFFFFFu, ref, k) >> 3;
+            VPL_DCHECK(tri >= 0 && tri < bv.n);
+            const float4* tr = bv.tris + 3 * tri;
+            const unsigned h = mt_segs<kCount>(x, S, S.pend, tmin, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), st);
+            S.occ |= h;
+            S.pend &= ~h;
+            if (h) cache.found(tri);
+            if (!__any_sync(0xFFFFFFFFu, S.pend != 0)) return;
+        }
+    }
+}
+
 // Resolve the pending segments of a group: beam over the group, else one beam
 // per VPL, else per-ray packets.  yk: the group's VPL positions (uniform).
 template <bool kCount>
 __device__ __forceinline__ void resolve_group(const BvhView& bv, f3 x, Segs& S, float eps, const f3* yk, int g,
-                                              OccluderCache& cache, int* __restrict__ sstack, TravStats* st) {
+                                              OccluderCache& cache, int* __restrict__ sstack, TravStats* st,
+                                              int& cand, int& cand_end, int cend, bool part,
+                                              const vpl_record* __restrict__ vpls, int i) {
     const int lane = threadIdx.x & 31;
     unsigned kany = 0;   // VPLs with a pending segment in some lane (uniform)
 #pragma unroll
@@ -291,7 +492,17 @@ __device__ __forceinline__ void resolve_group(const BvhView& bv, f3 x, Segs& S, 
     Beam B;
     if (make_beam(x, yk, S.pend, kany, eps, B)) {
         if (kCount && lane == 0) st->cpk += 1;
-        beam_traverse<kCount>(bv, x, S, eps, B, B.pos, cache, sstack, st);
+        if (VPL_CANDS && kGroup == 1 && i >= cand_end) {
+            cand_end = min(i + VPL_CAND_GROUP, cend);
+            cand = build_cands<kCount>(bv, x, part, vpls + i, cand_end - i, eps, sstack, st);
+            if (kCount && lane == 0) { if (cand >= 0) { st->lists += 1; st->entries += cand; } else st->lfail += 1; }
+        }
+        // the list covers the participating receivers only (the cluster cull is conservative, so a lane
+        // with a pending segment always participates; checked anyway)
+        if (VPL_CANDS && kGroup == 1 && cand >= 0 && !__any_sync(0xFFFFFFFFu, S.pend && !part))
+            filter_cands<kCount>(bv, x, S, eps, B, sstack, cand, cache, st);
+        else
+            beam_traverse<kCount>(bv, x, S, eps, B, B.pos, cache, sstack, st);
     } else {
         // loose: one beam per VPL of the group, loose single beams go per ray
         const bool several = kGroup > 1 && __popc(kany) > 1;   // compile-time false for single-VPL groups
@@ -362,7 +573,8 @@ __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_rec
                                                 const f3* yk, const int* yt, f3 x, f3 nx, int tri_x, bool active,
                                                 float eps,
                                                 float b2, OccluderCache& cache, int* __restrict__ sstack,
-                                                TravStats* st, float* w) {
+                                                TravStats* st, float* w, int& cand, int& cand_end, int cend,
+                                                bool part) {
     Segs S;
     S.pend = 0; S.occ = 0;
     unsigned traced = 0;
@@ -407,7 +619,7 @@ __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_rec
     S.pend |= keep_pend;
 #endif
     if (kCount) { st->chits += __popc(S.occ); st->ctests += st->tris - t0; }
-    resolve_group<kCount>(bv, x, S, eps, yk, g, cache, sstack, st);
+    resolve_group<kCount>(bv, x, S, eps, yk, g, cache, sstack, st, cand, cand_end, cend, part, vpls, i);
     const unsigned vis = traced & ~S.occ;
 #if VPL_CACHE_STREAK
     if (traced) cache.vis_streak = (vis == traced);

@@ -124,17 +124,18 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 float part[3] = {0.0f, 0.0f, 0.0f};
                 const int i1 = min(vend, i0 + 256);
                 for (int c0 = i0; c0 < i1; c0 += kCluster) {       // clusters of kCluster VPLs (i0 % 256 == 0)
-                    if (clusters &&
-                        !__any_sync(0xFFFFFFFFu, active && cluster_may_trace(clusters + 4 * (c0 / kCluster), x, nx)))
-                        continue;                                      // no lane can trace any VPL of it
+                    const float4* cb = clusters ? clusters + 4 * (c0 / kCluster) : nullptr;
+                    const bool inc = active && (!cb || cluster_may_trace(cb, x, nx));   // lane may trace it
+                    if (cb && !__any_sync(0xFFFFFFFFu, inc)) continue;   // no lane can trace any VPL of it
                     const int c1 = min(c0 + kCluster, i1);
+                    int cand = -1, cand_end = cb ? c0 : INT_MAX;           // candidate list (lazy) and its VPL range end
                     for (int i = c0; i < c1;) {
                         f3 yk[kGroup];
                         int yt[kGroup];
                         const int gsz = group_at(vpls, i, c1, xr, yk, yt);
                         float w[kGroup];
                         const unsigned tv = shade_group<kCount>(bv, vpls, i, gsz, yk, yt, x, nx, tri_x, active, eps, b2,
-                                                                cache, sstack, &st, w);
+                                                                cache, sstack, &st, w, cand, cand_end, c1, inc);
                         const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
                         if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
 #pragma unroll
@@ -199,10 +200,11 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
         }
         if (kCount) {
             unsigned long long pairs = active ? (unsigned long long)(vend - vbeg) : 0ull;
-            unsigned long long v[12] = {pairs, n_traced, n_vis, st.boxes, st.tris, st.wrays, st.wsteps,
-                                        st.cones, st.cpk, st.rpk, st.chits, st.ctests};
+            unsigned long long v[17] = {pairs, n_traced, n_vis, st.boxes, st.tris, st.wrays, st.wsteps,
+                                        st.cones, st.cpk, st.rpk, st.chits, st.ctests, st.lists, st.entries,
+                                        st.lfail, st.fsteps, st.lsteps};
 #pragma unroll
-            for (int q = 0; q < 12; ++q) {
+            for (int q = 0; q < 17; ++q) {
                 unsigned long long a = v[q];
                 for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
                 if (lane == 0) atomicAdd(&ctr->pairs + q, a);
@@ -241,8 +243,9 @@ __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict
             int yt[kGroup];
             const int gsz = group_at(vpls, i, i1, xr, yk, yt);
             float w[kGroup];
+            int cand = -1, cand_end = INT_MAX;   // the visibility dump walks the caller's order: tree traversal only
             const unsigned tv = shade_group<false>(bv, vpls, i, gsz, yk, yt, x, nx, tri_x, active, eps, b2, cache, sstack,
-                                                   nullptr, w);
+                                                   nullptr, w, cand, cand_end, i1, active);
             const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
             tb |= tr << (i - i0);
             vb |= vis << (i - i0);
