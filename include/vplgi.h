@@ -223,6 +223,22 @@ VPL_API int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, cons
                             int32_t tile_w, int32_t tile_h, float* d_rgb, vpl_counters* d_ctr, void* d_work,
                             size_t work_bytes, void* stream);
 
+/* test hook: the production gather (same launch as vpl_gather_indirect,
+ * counter build) that also records its own traced / visible bit of every
+ * (listed pixel, VPL) pair.  d_pixel_slot: int32[W*H] (nullable: no bits),
+ * the dump row of each pixel or -1; d_traced_bits / d_vis_bits:
+ * uint32[rows * ceil(n_vpls/32)], zeroed by the caller, bit i%32 of word i/32
+ * = VPL i of d_vpls (the caller's order).  d_ctr nullable.  flags:
+ * VPL_GATHER_NO_CULL runs without the VPL-cluster cull and the candidate
+ * lists (plain per-VPL beam traversal), so the counters of the two runs can
+ * be compared. */
+enum { VPL_GATHER_NO_CULL = 1 };
+VPL_API int32_t vpl_gather_dump(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf,
+                                const vpl_record* d_vpls, int32_t n_vpls, const int32_t* d_tiles, int32_t n_tiles,
+                                int32_t tile_w, int32_t tile_h, float* d_rgb, vpl_counters* d_ctr, void* d_work,
+                                size_t work_bytes, const int32_t* d_pixel_slot, uint32_t* d_traced_bits,
+                                uint32_t* d_vis_bits, int32_t flags, void* stream);
+
 /* NEXT f2  render_direct: the direct term L_e of Eq. 1 ("L_e(y)
  * represents direct illumination"; SPEC shade_direct S:327-335; O14,
  * reading R21) for the listed tiles: per pixel, `samples` uniform points on

@@ -24,7 +24,7 @@ EXPORTS = ["vpl_abi_version", "vpl_status_string", "vpl_last_error", "vpl_launch
            "vpl_scene_upload", "vpl_scene_consts", "vpl_scene_tri_data", "vpl_bvh_bytes", "vpl_build_bvh", "vpl_classify_near_far",
            "vpl_generate_bytes", "vpl_generate_vpls", "vpl_render_gbuffer", "vpl_gather_bytes",
            "vpl_gather_indirect", "vpl_render_direct", "vpl_image_error", "vpl_rejection_bytes",
-           "vpl_generate_rejection", "vpl_generate_metropolis", "vpl_visibility_dump", "vpl_closest_hit_batch", "vpl_occluded_batch",
+           "vpl_generate_rejection", "vpl_generate_metropolis", "vpl_visibility_dump", "vpl_gather_dump", "vpl_closest_hit_batch", "vpl_occluded_batch",
            "vpl_philox_batch"]
 
 
@@ -106,6 +106,7 @@ def load_library(path: str | os.PathLike | None = None):
         "vpl_generate_metropolis": (I32, [P, P, P, I64, I64, I64, I64, I64, C.c_uint64, P, P, P, P, P, SZ, P]),
         "vpl_generate_rejection": (I32, [P, P, P, I64, I64, C.c_uint64, P, P, P, P, P, P, P, SZ, P]),
         "vpl_visibility_dump": (I32, [P, P, P, P, I32, P, I32, P, P, P]),
+        "vpl_gather_dump": (I32, [P, P, P, P, I32, P, I32, I32, I32, P, P, P, SZ, P, P, P, I32, P]),
         "vpl_closest_hit_batch": (I32, [P, P, P, P, I64, F, F, P, P, P]),
         "vpl_occluded_batch": (I32, [P, P, P, P, I64, P, P]),
         "vpl_philox_batch": (I32, [P, I64, P, P]),
@@ -287,6 +288,39 @@ def gather_indirect(scene, bvh, gbuf, vpls, tiles, W, H, tw=16, th=16, rgb=None,
                                               tiles.numel(), tw, th, _ptr(rgb), _ptr(ctr), _ptr(work), work.numel(),
                                               _stream(stream)), "vpl_gather_indirect")
     return rgb, ctr
+
+
+def gather_dump(scene, bvh, gbuf, vpls, tiles, W, H, pixels=None, tw=16, th=16, no_cull=False, stream=None):
+    """Test hook: the production gather (vpl_gather_dump, counter build) plus its own traced / visible
+    bits for `pixels` (pixel indices, or None for counters only); no_cull=True runs it without the
+    VPL-cluster cull and candidate lists.  Returns (rgb, counters, traced_bits, vis_bits), the bit
+    arrays uint32 [len(pixels), ceil(M/32)] on the host (bit i = VPL i of `vpls`) or None."""
+    dev = scene.device
+    rgb = torch.zeros(H * W * 3, dtype=torch.float32, device=dev)
+    nv = vpls.shape[0] if vpls.dim() == 2 else vpls.numel() // VPL_RECORD_BYTES
+    wb = C.c_size_t()
+    _check(load_library().vpl_gather_bytes(nv, W, H, C.byref(wb)), "vpl_gather_bytes")
+    work = torch.empty(wb.value, dtype=torch.uint8, device=dev)
+    ctr = torch.zeros(len(COUNTER_NAMES), dtype=torch.int64, device=dev)
+    words = (nv + 31) // 32
+    slot = tb = vb = None
+    if pixels is not None:
+        px = np.asarray(pixels, np.int64)
+        slot = torch.full((H * W,), -1, dtype=torch.int32)
+        slot[torch.from_numpy(px)] = torch.arange(len(px), dtype=torch.int32)
+        slot = slot.to(dev)
+        tb = torch.zeros(len(px) * words, dtype=torch.int32, device=dev)
+        vb = torch.zeros(len(px) * words, dtype=torch.int32, device=dev)
+    _check(load_library().vpl_gather_dump(_ptr(scene), _ptr(bvh), _ptr(gbuf), _ptr(vpls), nv, _ptr(tiles),
+                                          tiles.numel(), tw, th, _ptr(rgb), _ptr(ctr), _ptr(work), work.numel(),
+                                          _ptr(slot), _ptr(tb), _ptr(vb), 1 if no_cull else 0, _stream(stream)),
+           "vpl_gather_dump")
+    torch.cuda.synchronize(dev)
+    if pixels is None:
+        return rgb, ctr, None, None
+    n = len(pixels)
+    return (rgb, ctr, tb.cpu().numpy().view(np.uint32).reshape(n, words),
+            vb.cpu().numpy().view(np.uint32).reshape(n, words))
 
 
 def render_direct(scene, bvh, gbuf, tiles, W, H, tw=16, th=16, samples=16, seed=0, rgb=None, accumulate=False,

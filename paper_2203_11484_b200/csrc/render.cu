@@ -80,12 +80,21 @@ __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, floa
 #ifndef VPL_GATHER_CTAS
 #define VPL_GATHER_CTAS 32
 #endif
-template <bool kCount>
+// Test hook (kDump, vpl_gather_dump): the production gather additionally records, for listed pixels,
+// its own traced / visible bit of every pixel x VPL pair (indexed by the caller's VPL order through
+// the sort permutation) — the visibility the image was computed with.
+struct GatherDump {
+    const int32_t* slot;   // [W*H] pixel -> dump row, -1 = not dumped
+    const int32_t* perm;   // sorted position -> caller's VPL index (null: identity)
+    uint32_t *tbits, *vbits;
+    int32_t words;         // ceil(M / 32)
+};
+template <bool kCount, bool kDump = false>
 __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint* __restrict__ gb,
                                                 const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
                                                 vpl_counters* __restrict__ ctr, int* __restrict__ queue,
                                                 const float4* __restrict__ clusters, int32_t chunk, int32_t n_chunks,
-                                                float* __restrict__ part_out, int* __restrict__ done) {
+                                                float* __restrict__ part_out, int* __restrict__ done, GatherDump dump) {
     __shared__ int sstack[kWarpStack];
     __shared__ float s_acc[3][32];   // running per-lane totals (kept out of the register budget)
     const int lane = threadIdx.x;
@@ -104,6 +113,8 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
         bool active = false;
         f3 x = mk3(0, 0, 0), nx = mk3(0, 0, 0);
         int tri_x = -1;
+        int dslot = -1;
+        if (kDump && pix >= 0) dslot = dump.slot[pix];
         if (pix >= 0) {
             const float4* gp = (const float4*)(gb + pix);
             float4 a = gp[0], b = gp[1];
@@ -138,6 +149,14 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                                                                 cache, sstack, &st, w, cand, cand_end, c1, inc);
                         const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
                         if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
+                        if (kDump && dslot >= 0) {
+                            for (int k = 0; k < gsz; ++k) {
+                                const int o = dump.perm ? dump.perm[i + k] : i + k;
+                                const size_t wd = (size_t)dslot * dump.words + (o >> 5);
+                                if (tr & (1u << k)) atomicOr(dump.tbits + wd, 1u << (o & 31));
+                                if (vis & (1u << k)) atomicOr(dump.vbits + wd, 1u << (o & 31));
+                            }
+                        }
 #pragma unroll
                         for (int k = 0; k < kGroup; ++k) {
                             if (vis & (1u << k)) {
@@ -507,9 +526,10 @@ int32_t vpl_gather_bytes(int32_t n_vpls, int32_t width, int32_t height, size_t* 
     return VPL_OK;
 }
 
-int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf, const vpl_record* d_vpls,
-                            int32_t n_vpls, const int32_t* d_tiles, int32_t n_tiles, int32_t tile_w, int32_t tile_h,
-                            float* d_rgb, vpl_counters* d_ctr, void* d_work, size_t work_bytes, void* stream) {
+static int32_t gather_impl(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf, const vpl_record* d_vpls,
+                           int32_t n_vpls, const int32_t* d_tiles, int32_t n_tiles, int32_t tile_w, int32_t tile_h,
+                           float* d_rgb, vpl_counters* d_ctr, void* d_work, size_t work_bytes, void* stream,
+                           GatherDump dump, int32_t flags = 0) {
     if (!d_scene || !d_bvh || !d_gbuf || !d_rgb || !d_work || n_vpls < 0 || (n_vpls > 0 && !d_vpls)) {
         set_error("vpl_gather_indirect: bad arguments");
         return VPL_EINVAL;
@@ -533,6 +553,7 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
     if (n_chunks > 1)
         VPL_CUDA(cudaMemsetAsync(w.done, 0, sizeof(int) * (size_t)((hh.W + 7) / 8) * (size_t)((hh.H + 3) / 4), s));
     const vpl_record* vp = d_vpls;
+    dump.perm = nullptr;
     if (n_vpls > 1) {
         const unsigned init[6] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u, 0u};
         VPL_CUDA(cudaMemcpyAsync(w.box, init, sizeof(init), cudaMemcpyHostToDevice, s));
@@ -545,10 +566,11 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
         k_vpl_permute<<<nb(n_vpls, 256), 256, 0, s>>>(d_vpls, w.idx2, n_vpls, w.sorted);
         VPL_LAUNCHED("k_vpl_permute");
         vp = w.sorted;
+        dump.perm = w.idx2;
     }
     const float4* clusters = nullptr;
 #if VPL_CLUSTER_CULL
-    if (n_vpls > 0) {
+    if (n_vpls > 0 && !(flags & VPL_GATHER_NO_CULL)) {
         const int ncl = (n_vpls + kCluster - 1) / kCluster;
         k_vpl_clusters<<<nb(ncl, 128), 128, 0, s>>>(vp, n_vpls, w.clusters);
         VPL_LAUNCHED("k_vpl_clusters");
@@ -566,16 +588,42 @@ int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gp
     VPL_CUDA(cudaFuncSetAttribute(k_gather<false>, cudaFuncAttributePreferredSharedMemoryCarveout, VPL_CARVEOUT));
     VPL_CUDA(cudaFuncSetAttribute(k_gather<true>, cudaFuncAttributePreferredSharedMemoryCarveout, VPL_CARVEOUT));
 #endif
-    if (d_ctr)
+    if (dump.slot)
+        k_gather<true, true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue, clusters, chunk,
+                                                  n_chunks, w.part, w.done, dump);
+    else if (d_ctr)
         k_gather<true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue, clusters, chunk,
-                                            n_chunks, w.part, w.done);
+                                            n_chunks, w.part, w.done, dump);
     else
         k_gather<false><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue, clusters, chunk,
-                                             n_chunks, w.part, w.done);
+                                             n_chunks, w.part, w.done, dump);
     VPL_LAUNCHED("k_gather");
 
     return VPL_OK;
 }
+
+int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf, const vpl_record* d_vpls,
+                            int32_t n_vpls, const int32_t* d_tiles, int32_t n_tiles, int32_t tile_w, int32_t tile_h,
+                            float* d_rgb, vpl_counters* d_ctr, void* d_work, size_t work_bytes, void* stream) {
+    GatherDump dump{nullptr, nullptr, nullptr, nullptr, 0};
+    return gather_impl(d_scene, d_bvh, d_gbuf, d_vpls, n_vpls, d_tiles, n_tiles, tile_w, tile_h, d_rgb, d_ctr, d_work,
+                       work_bytes, stream, dump);
+}
+
+int32_t vpl_gather_dump(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf, const vpl_record* d_vpls,
+                        int32_t n_vpls, const int32_t* d_tiles, int32_t n_tiles, int32_t tile_w, int32_t tile_h,
+                        float* d_rgb, vpl_counters* d_ctr, void* d_work, size_t work_bytes,
+                        const int32_t* d_pixel_slot, uint32_t* d_traced_bits, uint32_t* d_vis_bits, int32_t flags,
+                        void* stream) {
+    if ((d_pixel_slot && (!d_traced_bits || !d_vis_bits)) || n_vpls <= 0 || (flags & ~VPL_GATHER_NO_CULL)) {
+        set_error("vpl_gather_dump: bad arguments");
+        return VPL_EINVAL;
+    }
+    GatherDump dump{d_pixel_slot, nullptr, d_traced_bits, d_vis_bits, (n_vpls + 31) / 32};
+    return gather_impl(d_scene, d_bvh, d_gbuf, d_vpls, n_vpls, d_tiles, n_tiles, tile_w, tile_h, d_rgb, d_ctr, d_work,
+                       work_bytes, stream, dump, flags);
+}
+
 
 int32_t vpl_render_direct(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf, const int32_t* d_tiles,
                           int32_t n_tiles, int32_t tile_w, int32_t tile_h, int32_t samples, uint64_t seed,
