@@ -59,6 +59,12 @@ namespace vplgi {
 #define VPL_CAND_GROUP 16     // a list covers the next VPL_CAND_GROUP VPLs of the cluster from the first that needs it
                               // (C4: 8 / 12 / 16 / 24 / 32 measured, 16 best)
 #endif
+#ifndef VPL_CAND_TOL_PCT
+#define VPL_CAND_TOL_PCT 0    // > 0: adaptive runs (box extent < VPL_CAND_TOL_PCT % of the distance), <= VPL_CAND_GROUP long
+#endif
+#ifndef VPL_CAND_MINRUN
+#define VPL_CAND_MINRUN 2     // shorter adaptive runs get no list (per-VPL traversal)
+#endif
 #ifndef VPL_CAND_STRADDLE
 #define VPL_CAND_STRADDLE 1   // 1: also build lists for beams with straddling axes (extent test; C4 -3%)
 #endif
@@ -236,13 +242,15 @@ struct ClusterBeam {
     Beam B;
     float L[3], U[3];
 };
-__device__ __forceinline__ bool make_cluster_beam(f3 x, bool part, float4 ylo, float4 yhi, float eps, ClusterBeam& C) {
+// xl / xh: the box of the participating receivers (warp reductions); D = x - y over the two boxes is
+// [xl - yh, xh - yl] (fp32 subtraction is monotonic in each operand, so every lane's rounded D is inside).
+__device__ __forceinline__ bool make_cluster_beam(const float* xl, const float* xh, float4 ylo, float4 yhi, float eps,
+                                                  ClusterBeam& C) {
     const float inf = __int_as_float(0x7f800000);
     const float yl[3] = {ylo.x, ylo.y, ylo.z}, yh[3] = {yhi.x, yhi.y, yhi.z};
     float Dn[3], Dm[3];
-    Dn[0] = warp_min_f32(part ? x.x - yhi.x : inf); Dm[0] = warp_max_f32(part ? x.x - ylo.x : -inf);
-    Dn[1] = warp_min_f32(part ? x.y - yhi.y : inf); Dm[1] = warp_max_f32(part ? x.y - ylo.y : -inf);
-    Dn[2] = warp_min_f32(part ? x.z - yhi.z : inf); Dm[2] = warp_max_f32(part ? x.z - ylo.z : -inf);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { Dn[a] = xl[a] - yh[a]; Dm[a] = xh[a] - yl[a]; }
     float l2n = 0.0f, l2m = 0.0f;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {   // |D| over the box: per axis the nearer / farther face
@@ -373,17 +381,51 @@ __device__ __noinline__
 __device__ __forceinline__
 #endif
 int build_cands(const BvhView& bv, f3 x, bool part, const vpl_record* __restrict__ vg, int ng, float eps,
-                                        int* __restrict__ sstack, TravStats* st) {
+                                        int* __restrict__ sstack, TravStats* st, int& run) {
     const int lane = threadIdx.x & 31;
+    run = ng;
     if (bv.root < 0) return -1;
-    // position box of the ng VPLs vg[0..ng) (lane l loads VPL l)
     const float inf = __int_as_float(0x7f800000);
+    const float xl[3] = {warp_min_f32(part ? x.x : inf), warp_min_f32(part ? x.y : inf), warp_min_f32(part ? x.z : inf)};
+    const float xh[3] = {warp_max_f32(part ? x.x : -inf), warp_max_f32(part ? x.y : -inf),
+                         warp_max_f32(part ? x.z : -inf)};
+    // position box of the run vg[0..run) (lane l loads VPL l)
     float4 ylo = make_float4(inf, inf, inf, 0.0f), yhi = make_float4(-inf, -inf, -inf, 0.0f);
     if (lane < ng) { const float4 p = __ldg((const float4*)(vg + lane)); ylo = p; yhi = p; }
+#if VPL_CAND_TOL_PCT > 0
+    {   // adaptive run: the longest prefix whose box stays within VPL_CAND_TOL_PCT % of the distance from its first
+        // VPL to the receivers (inclusive prefix min / max over the lanes)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float a0 = __shfl_up_sync(0xFFFFFFFFu, ylo.x, o), a1 = __shfl_up_sync(0xFFFFFFFFu, ylo.y, o);
+            const float a2 = __shfl_up_sync(0xFFFFFFFFu, ylo.z, o), b0 = __shfl_up_sync(0xFFFFFFFFu, yhi.x, o);
+            const float b1 = __shfl_up_sync(0xFFFFFFFFu, yhi.y, o), b2 = __shfl_up_sync(0xFFFFFFFFu, yhi.z, o);
+            if (lane >= o) {
+                ylo.x = fminf(ylo.x, a0); ylo.y = fminf(ylo.y, a1); ylo.z = fminf(ylo.z, a2);
+                yhi.x = fmaxf(yhi.x, b0); yhi.y = fmaxf(yhi.y, b1); yhi.z = fmaxf(yhi.z, b2);
+            }
+        }
+        const float y0x = __shfl_sync(0xFFFFFFFFu, ylo.x, 0), y0y = __shfl_sync(0xFFFFFFFFu, ylo.y, 0),
+                    y0z = __shfl_sync(0xFFFFFFFFu, ylo.z, 0);
+        const float cx = 0.5f * (xl[0] + xh[0]) - y0x, cy = 0.5f * (xl[1] + xh[1]) - y0y,
+                    cz = 0.5f * (xl[2] + xh[2]) - y0z;
+        constexpr float kTol = VPL_CAND_TOL_PCT * 0.01f;
+        const float lim2 = (kTol * kTol) * ((cx * cx + cy * cy) + cz * cz);
+        const float ext = fmax3(yhi.x - ylo.x, yhi.y - ylo.y, yhi.z - ylo.z);
+        const unsigned bad = __ballot_sync(0xFFFFFFFFu, lane < ng && !(ext * ext < lim2));
+        run = bad ? min(ng, __ffs(bad) - 1) : ng;
+        if (run < VPL_CAND_MINRUN) { run = 1; return -1; }
+        const int l = run - 1;
+        ylo.x = __shfl_sync(0xFFFFFFFFu, ylo.x, l); ylo.y = __shfl_sync(0xFFFFFFFFu, ylo.y, l);
+        ylo.z = __shfl_sync(0xFFFFFFFFu, ylo.z, l); yhi.x = __shfl_sync(0xFFFFFFFFu, yhi.x, l);
+        yhi.y = __shfl_sync(0xFFFFFFFFu, yhi.y, l); yhi.z = __shfl_sync(0xFFFFFFFFu, yhi.z, l);
+    }
+#else
     ylo.x = warp_min_f32(ylo.x); ylo.y = warp_min_f32(ylo.y); ylo.z = warp_min_f32(ylo.z);
     yhi.x = warp_max_f32(yhi.x); yhi.y = warp_max_f32(yhi.y); yhi.z = warp_max_f32(yhi.z);
+#endif
     ClusterBeam CB;
-    if (!make_cluster_beam(x, part, ylo, yhi, eps, CB)) return -1;
+    if (!make_cluster_beam(xl, xh, ylo, yhi, eps, CB)) return -1;
     const int half = lane >> 4;
     const unsigned below = (1u << lane) - 1u;
     const unsigned hmask = half ? 0xFFFF0000u : 0x0000FFFFu;
@@ -493,8 +535,9 @@ __device__ __forceinline__ void resolve_group(const BvhView& bv, f3 x, Segs& S, 
     if (make_beam(x, yk, S.pend, kany, eps, B)) {
         if (kCount && lane == 0) st->cpk += 1;
         if (VPL_CANDS && kGroup == 1 && i >= cand_end) {
-            cand_end = min(i + VPL_CAND_GROUP, cend);
-            cand = build_cands<kCount>(bv, x, part, vpls + i, cand_end - i, eps, sstack, st);
+            int run;
+            cand = build_cands<kCount>(bv, x, part, vpls + i, min(VPL_CAND_GROUP, cend - i), eps, sstack, st, run);
+            cand_end = i + run;
             if (kCount && lane == 0) { if (cand >= 0) { st->lists += 1; st->entries += cand; } else st->lfail += 1; }
         }
         // the list covers the participating receivers only (the cluster cull is conservative, so a lane

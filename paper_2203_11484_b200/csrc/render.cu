@@ -80,6 +80,9 @@ __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, floa
 #ifndef VPL_GATHER_CTAS
 #define VPL_GATHER_CTAS 32
 #endif
+#ifndef VPL_PART_EVICT_LAST
+#define VPL_PART_EVICT_LAST 1   // partial stores with an L2 evict_last policy (C4: DRAM writes 120 -> 64 MB per launch)
+#endif
 // Test hook (kDump, vpl_gather_dump): the production gather additionally records, for listed pixels,
 // its own traced / visible bit of every pixel x VPL pair (indexed by the caller's VPL order through
 // the sort permutation) — the visibility the image was computed with.
@@ -94,7 +97,8 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                                                 const vpl_record* __restrict__ vpls, int32_t M, float* __restrict__ rgb,
                                                 vpl_counters* __restrict__ ctr, int* __restrict__ queue,
                                                 const float4* __restrict__ clusters, int32_t chunk, int32_t n_chunks,
-                                                float* __restrict__ part_out, int* __restrict__ done, GatherDump dump) {
+                                                float* __restrict__ part_out, int* __restrict__ done,
+                                                int* __restrict__ slot_gen, int32_t ring, GatherDump dump) {
     __shared__ int sstack[kWarpStack];
     __shared__ float s_acc[3][32];   // running per-lane totals (kept out of the register budget)
     const int lane = threadIdx.x;
@@ -182,20 +186,40 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 o[2] = active ? s_acc[2][lane] * rho.z * s : 0.0f;
             }
         }
-        const int64_t blk = n_chunks > 1 ? tm.block_index(g / n_chunks) : -1;
-        VPL_DCHECK(blk < (int64_t)((tm.W + 7) / 8) * ((tm.H + 3) / 4));
         VPL_DCHECK(pix < (int64_t)tm.W * tm.H);
-        if (blk >= 0) {
-            // chunk partial sums, (block, chunk, lane)-contiguous; the warp that completes a block's last
-            // chunk folds them in chunk order (fp32) while they are still in L2, writes the pixels and
-            // discards the partial lines so they are never written back to HBM
-            float* pb = part_out + (blk * n_chunks) * 96;             // 96 floats = 32 lanes x 3 = 3 lines
+        if (n_chunks > 1) {
+            // chunk partial sums, (slot, chunk, lane)-contiguous in a ring of `ring` block slots (the
+            // call's block ordinal modulo ring: a few MB stay L2-resident); the warp that completes a
+            // block's last chunk folds them in chunk order (fp32), writes the pixels, discards the
+            // partial lines (never written back to HBM) and hands the slot to the block `ring` later.
+            const int64_t lb = g / n_chunks;
+            const int slot = (int)(lb % ring), gen = (int)(lb / ring);
+            float* pb = part_out + ((int64_t)slot * n_chunks) * 96;   // 96 floats = 32 lanes x 3 = 3 lines
+            if (lane == 0) {   // the slot's previous block (dispensed earlier, so running) must be folded
+                int cur;
+                while (true) {
+                    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(cur) : "l"(slot_gen + slot) : "memory");
+                    if (cur >= gen) break;
+                    __nanosleep(256);
+                }
+            }
+            __syncwarp();
             float* o = pb + ch * 96 + 3 * lane;
+#if VPL_PART_EVICT_LAST
+            {   // keep the partial lines in L2 until the fold discards them
+                uint64_t pol;
+                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+                asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(o), "f"(s_acc[0][lane]), "l"(pol) : "memory");
+                asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(o + 1), "f"(s_acc[1][lane]), "l"(pol) : "memory");
+                asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(o + 2), "f"(s_acc[2][lane]), "l"(pol) : "memory");
+            }
+#else
             o[0] = s_acc[0][lane]; o[1] = s_acc[1][lane]; o[2] = s_acc[2][lane];
+#endif
             __threadfence();
             __syncwarp();
             int prev = 0;
-            if (lane == 0) prev = atomicAdd(done + blk, 1);
+            if (lane == 0) prev = atomicAdd(done + slot, 1);
             prev = __shfl_sync(0xFFFFFFFFu, prev, 0);
             if (prev == n_chunks - 1) {
                 __threadfence();
@@ -215,6 +239,12 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 __syncwarp();
                 for (int l = lane; l < 3 * n_chunks; l += 32)
                     asm volatile("discard.global.L2 [%0], 128;" ::"l"(pb + 32 * l) : "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    done[slot] = 0;
+                    __threadfence();
+                    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(slot_gen + slot), "r"(gen + 1) : "memory");
+                }
             }
         }
         if (kCount) {
@@ -448,6 +478,8 @@ static inline void gather_chunks(int32_t M, int32_t* chunk, int32_t* n_chunks) {
 
 struct GatherWork {
     int* queue;
+    int* slot_gen;
+    int32_t ring;
     unsigned* box;
     float4* clusters;
     float* part;
@@ -458,14 +490,22 @@ struct GatherWork {
     void* cub;
     size_t cub_bytes;
 };
+// partial-sum ring: block slots reused modulo VPL_PART_RING (C4: 4096 x 128 chunks x 384 B = 201 MB
+// allocated instead of 3.2 GB for the whole frame; 512 slots made warps wait on straggler chunks: +30%)
+#ifndef VPL_PART_RING
+#define VPL_PART_RING 4096
+#endif
+
 static size_t gather_layout(int32_t M, int32_t W, int32_t H, char* base, GatherWork* w) {
     Bump b{base};
     w->queue = b.take<int>(1);
     int32_t chunk, nch;
     gather_chunks(M, &chunk, &nch);
     const size_t nblk = (size_t)((W + 7) / 8) * (size_t)((H + 3) / 4);   // 8x4 blocks of a full frame
-    w->part = b.take<float>(nch > 1 ? nblk * (size_t)nch * 96 : 1);
-    w->done = b.take<int>(nblk);
+    w->ring = (int32_t)(nblk < (size_t)VPL_PART_RING ? (nblk > 0 ? nblk : 1) : VPL_PART_RING);
+    w->part = b.take<float>(nch > 1 ? (size_t)w->ring * (size_t)nch * 96 : 1);
+    w->done = b.take<int>(w->ring);
+    w->slot_gen = b.take<int>(w->ring);
     w->box = b.take<unsigned>(6);
     size_t m = (size_t)(M > 0 ? M : 1);
     w->keys = b.take<uint32_t>(m);
@@ -550,8 +590,10 @@ static int32_t gather_impl(const void* d_scene, const void* d_bvh, const vpl_gpo
     if (n_tiles == 0) return VPL_OK;
     int* queue = w.queue;
     VPL_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
-    if (n_chunks > 1)
-        VPL_CUDA(cudaMemsetAsync(w.done, 0, sizeof(int) * (size_t)((hh.W + 7) / 8) * (size_t)((hh.H + 3) / 4), s));
+    if (n_chunks > 1) {
+        VPL_CUDA(cudaMemsetAsync(w.done, 0, sizeof(int) * (size_t)w.ring, s));
+        VPL_CUDA(cudaMemsetAsync(w.slot_gen, 0, sizeof(int) * (size_t)w.ring, s));
+    }
     const vpl_record* vp = d_vpls;
     dump.perm = nullptr;
     if (n_vpls > 1) {
@@ -590,13 +632,13 @@ static int32_t gather_impl(const void* d_scene, const void* d_bvh, const vpl_gpo
 #endif
     if (dump.slot)
         k_gather<true, true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue, clusters, chunk,
-                                                  n_chunks, w.part, w.done, dump);
+                                                  n_chunks, w.part, w.done, w.slot_gen, w.ring, dump);
     else if (d_ctr)
         k_gather<true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue, clusters, chunk,
-                                            n_chunks, w.part, w.done, dump);
+                                            n_chunks, w.part, w.done, w.slot_gen, w.ring, dump);
     else
         k_gather<false><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue, clusters, chunk,
-                                             n_chunks, w.part, w.done, dump);
+                                             n_chunks, w.part, w.done, w.slot_gen, w.ring, dump);
     VPL_LAUNCHED("k_gather");
 
     return VPL_OK;
