@@ -94,52 +94,77 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- algorithmic op counts
-# Per-unit thread-op counts: the arithmetic the method itself prescribes per
-# unit of work, split by the SM pipe that executes it.  The
-# exact fp32 contract (O0) forbids FMA contraction in the Eq. 1 terms and the
-# segment setup, so those count as separate FMUL/FADD; the any-hit MT counts
-# the fused form of reading R26; square roots and divisions count as one MUFU
-# op each.  (fma, alu, mufu) per unit:
-OPS = {"pairs": (14, 3, 0),       # d (3), r^2 (5), cx (3, fused), ci (3, fused) | tri, cx, ci tests (O13, R26)
-       "traced": (9, 2, 2),       # tmax, cx*ci, r2*max, 3 FFMA, d*inv (3) | test, max | sqrt, 1/dist  (O9, O13, R25)
-       "box_tests": (12, 5, 0),   # per-ray slab (centre/half-extent): 3 FFMA + 3 FMUL + 6 FADD | 4 min/max + cmp
-       "cone_tests": (6, 11, 0),  # beam x child box: 6 FFMA | 6 SEL + 4 min/max + 1 cmp (gather.cuh beam_box)
-       "tri_tests": (30, 9, 0)}   # exact MT any hit (O9, R25, R26): 27 FMUL/FFMA/FADD + a_u+a_v, tmin*D, tmax*D | 6 compares + 3 sign flips
+# SURVEY §8(d)'s per-unit algorithmic cost (what the method must compute,
+# excluding traversal control), thread-ops split by SM pipe, and bytes the
+# unit requests from L2:   unit: (FMA pipe, ALU pipe, MUFU, L2 bytes)
+OPS = {"pairs": (12, 2, 0, 0),        # every pair: d, r^2, 2 dots, cull (VPL record from smem / L1, amortised)
+       "traced": (14, 1, 5, 0),       # traced pair: G, shadow-ray setup, accumulate
+       "box_tests": (6, 11, 0, 32),   # per-ray child-box test (4-wide node: 32 B per child)
+       "cone_tests": (6, 11, 0, 32),  # beam x child box (16-wide node child, or a list entry: 32 B)
+       "tri_tests": (27, 7, 1, 48)}   # exact Moller-Trumbore test (triangle: 48 B)
 
-# Pipe rates in thread-ops per clock per SM, measured on this pool's B200
-# (tools/pipebench.cu, profiles/r01_pipebench.jsonl): FFMA/FMUL/FADD 126,
-# FMNMX/FSETP/FSEL/LOP3 64, MUFU.RCP 14.6; instruction issue 4 warps x 32.
+# Roof rates: thread-ops per clock per SM — FMA pipe 128, ALU
+# pipe 64 (FMNMX/FSETP/FSEL/LOP3, tools/pipebench.cu measured 63.7-64.0),
+# MUFU 16, instruction issue 4 x 32; L2 read bandwidth measured by
+# tools/pipebench.cu on this pool's B200 (profiles/r02_pipebench.jsonl).
 PIPE = {"fma": 128.0, "alu": 64.0, "mufu": 16.0, "issue": 128.0}
+FP32_PEAK_TFLOPS = 74.4   # BJ:5: 148 SMs x 128 FMA lanes x 2 flop x 1.965 GHz
 
 
-def algorithmic_ops(c: dict) -> int:
-    return sum(c[k] * sum(v) for k, v in OPS.items())
+def l2_bandwidth():
+    f = ROOT / "profiles" / "r02_pipebench.jsonl"
+    if f.exists():
+        for line in f.read_text().splitlines():
+            try:
+                d = json.loads(line)
+            except ValueError:
+                continue
+            if "GB_per_s" in d:
+                return float(d["GB_per_s"]) * 1e9
+    return None
 
 
-def roof_seconds(c: dict, sms: int, f_hz: float) -> tuple[float, str]:
-    """T_roof = max over pipes of ops / (rate * SMs * f); returns (T, binding pipe)."""
-    fma = sum(c[k] * v[0] for k, v in OPS.items())
-    alu = sum(c[k] * v[1] for k, v in OPS.items())
-    mufu = sum(c[k] * v[2] for k, v in OPS.items())
-    t = {"fma": fma / PIPE["fma"], "alu": alu / PIPE["alu"], "mufu": mufu / PIPE["mufu"],
-         "issue": (fma + alu + mufu) / PIPE["issue"]}
-    k = max(t, key=t.get)
-    return t[k] / (sms * f_hz), k
+def pipe_ops(c: dict) -> dict:
+    return {p: sum(c[k] * v[i] for k, v in OPS.items()) for i, p in enumerate(("fma", "alu", "mufu", "l2_bytes"))}
+
+
+def roof_terms(c: dict, sms: int, f_hz: float, l2_bps) -> dict:
+    """SURVEY §8(d): T_roof = max(FMA/(128 SMs f), ALU/(64 SMs f), MUFU/(16 SMs f), L2 bytes/BW_L2);
+    plus the issue limit (all ops / (128 SMs f)) that binds an issue-bound kernel."""
+    o = pipe_ops(c)
+    t = {"fma": o["fma"] / (PIPE["fma"] * sms * f_hz), "alu": o["alu"] / (PIPE["alu"] * sms * f_hz),
+         "mufu": o["mufu"] / (PIPE["mufu"] * sms * f_hz)}
+    if l2_bps:
+        t["l2"] = o["l2_bytes"] / l2_bps
+    t["issue"] = (o["fma"] + o["alu"] + o["mufu"]) / (PIPE["issue"] * sms * f_hz)
+    return t
+
+
+def sources_sha() -> str:
+    """Hash of the CUDA sources and the ABI header: stamps which kernel version a committed ncu capture measured."""
+    import hashlib
+    h = hashlib.sha256()
+    files = sorted((ROOT / "paper_2203_11484_b200" / "csrc").glob("*.cu*")) + [ROOT / "include" / "vplgi.h"]
+    for f in files:
+        h.update(f.name.encode())
+        h.update(f.read_bytes())
+    return h.hexdigest()[:12]
 
 
 def measured_traffic():
     """dram read + write bytes of one C4 gather launch from the committed ncu
-    capture (profiles/r01_gather_c4_dram.csv), or None."""
+    capture (profiles/gather_c4_dram.csv) and the source hash it was taken on
+    (profiles/gather_c4_dram.sha), or (None, None)."""
     import csv
-    f = ROOT / "profiles" / "r01_gather_c4_dram.csv"
+    f, st = ROOT / "profiles" / "gather_c4_dram.csv", ROOT / "profiles" / "gather_c4_dram.sha"
     if not f.exists():
-        return None
+        return None, None
     tot, seen = 0.0, 0
     for r in csv.reader(f.read_text().splitlines()):
         if len(r) > 14 and r[12] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             tot += float(r[14].replace(",", ""))
             seen += 1
-    return tot if seen == 2 else None
+    return (tot if seen == 2 else None), (st.read_text().strip() if st.exists() else None)
 
 
 # ---------------------------------------------------------------------------- our arm
@@ -167,11 +192,12 @@ def run_ours(args):
     V.load_library()
     s = scenegen.make_scene(args.config)
     W, H, tw, th = s.width, s.height, 16, 16
-    from paper_2203_11484_b200.parallel import tiles_for_rank
+    from paper_2203_11484_b200.parallel import FrameAssembler, tiles_for_rank
     tiles = tiles_for_rank(W, H, tw, th, rank, world, device=dev)
+    assembler = FrameAssembler(W, H, tw, th, world, device=dev)
     stream = torch.cuda.current_stream()
 
-    # inputs resident in HBM (rank 0 owns the scene; others receive it by broadcast each step)
+    # inputs resident in HBM (rank 0 owns the scene; the others receive it by broadcast)
     d_verts = torch.from_numpy(s.verts.reshape(-1)).to(dev)
     d_alb = torch.from_numpy(s.albedo.reshape(-1)).to(dev)
     r = V.Renderer(s, device=dev, tw=tw, th=th, tiles=tiles)
@@ -179,28 +205,27 @@ def run_ours(args):
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
     ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for k in ("step", "gather")}
-    state = {}
+          for k in ("step", "setup", "frame", "gather")}
 
-    def step(counters=False):
+    def setup():
+        """scene setup (reported separately): broadcast, a1 upload, a2 BVH build"""
         if world > 1:
-            # the frame is assembled by an in-place SUM all-reduce, so every rank's buffer
-            # holds the other ranks' tiles afterwards: they must start from zero every step
-            r.rgb.zero_()
             dist.broadcast(d_verts, 0)
             dist.broadcast(d_alb, 0)
         r.upload(d_verts, d_alb, stream)
         r.bvh, r._bwork = V.build_bvh(r.scene, r.n, r._bvh, r._bwork, stream)
         r._bvh = r.bvh
+
+    def frame(counters=False):
+        """per frame: a3-a6 on rank 0 + VPL broadcast, a7 G-buffer and a8 gather of the rank's tiles,
+        a9 framebuffer gather to rank 0"""
         if rank == 0:
             r.labels, r.n_near = V.classify_near_far(r.scene, r.n, s.T, stream=stream)
             r.vpls, r.info, r._gwork = V.generate_vpls(r.scene, r.bvh, r.labels, r.n, s.M, s.K_near, s.max_depth,
                                                       s.rr, s.seed, max_out=r.max_out, vpls=vbuf, work=r._gwork,
                                                       stream=stream)
-            nv = torch.tensor([r.info["n_out"]], dtype=torch.int64, device=dev)
-        else:
-            nv = torch.zeros(1, dtype=torch.int64, device=dev)
         if world > 1:
+            nv = torch.tensor([r.info["n_out"] if rank == 0 else 0], dtype=torch.int64, device=dev)
             dist.broadcast(nv, 0)
             n_out = int(nv.item())
             dist.broadcast(vbuf[: n_out * V.VPL_RECORD_BYTES], 0)
@@ -210,8 +235,17 @@ def run_ours(args):
         r.rgb, r.ctr = V.gather_indirect(r.scene, r.bvh, r.gbuf, r.vpls, r.tiles, W, H, tw, th, r.rgb, counters,
                                          stream=stream)
         ev["gather"][1].record(stream)
-        if world > 1:
-            dist.all_reduce(r.rgb, op=dist.ReduceOp.SUM)     # disjoint tiles: exact assembly on every rank
+        assembler(r.rgb, rank, dst=0)
+        return r.rgb
+
+    def step(counters=False):
+        """one pass of every §8(a) row: a1-a2 (setup) then a3-a9 (frame)"""
+        ev["setup"][0].record(stream)
+        setup()
+        ev["setup"][1].record(stream)
+        ev["frame"][0].record(stream)
+        frame(counters)
+        ev["frame"][1].record(stream)
         return r.rgb
 
     # pairs per step: front-hit pixels of the whole frame x VPLs
@@ -238,7 +272,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     launches0 = V.launch_count()
-    step_ms, gather_ms = [], []
+    times = {k: [] for k in ("step", "setup", "frame", "gather")}
     with ClockSampler(gpu) as clk:
         for _ in range(args.steps):
             flush.zero_()                                   # L2 flush between timed steps (untimed)
@@ -249,15 +283,17 @@ def run_ours(args):
             step()
             ev["step"][1].record(stream)
             torch.cuda.synchronize()
-            step_ms.append(ev["step"][0].elapsed_time(ev["step"][1]))
-            gather_ms.append(ev["gather"][0].elapsed_time(ev["gather"][1]))
+            for k in times:
+                times[k].append(ev[k][0].elapsed_time(ev[k][1]))
     launches = (V.launch_count() - launches0) / max(args.steps, 1)
-    t_step = sum(step_ms) / len(step_ms)
-    t_gather = sum(gather_ms) / len(gather_ms)
-    if world > 1:
-        tt = torch.tensor([t_step, t_gather], dtype=torch.float64, device=dev)
+    t = {k: sum(v) / len(v) for k, v in times.items()}
+    if world > 1:   # max over ranks
+        tt = torch.tensor([t[k] for k in times], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step, t_gather = (float(x) for x in tt.cpu())
+        t = dict(zip(times, (float(x) for x in tt.cpu())))
+    t_step, t_gather = t["step"], t["gather"]
+    if rank == 0 and os.environ.get("VPLGI_BENCH_DUMP"):     # assembled frame (tests compare 1 vs N ranks)
+        np.save(os.environ["VPLGI_BENCH_DUMP"], r.rgb.cpu().numpy())
 
     # e2e through the public API with host buffers: pinned H2D of the scene, D2H of the image
     h_verts = torch.from_numpy(s.verts.reshape(-1)).pin_memory()
@@ -291,15 +327,24 @@ def run_ours(args):
         cpu_base = cpu_baseline(s, r, args.cpu_seconds)
 
     if rank == 0:
-        peaks, peak_src = _peaks()
         sm_count = V.device_info()["sm_count"]
         clocks = clk.summary()
-        f_max = (clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
-        ops = algorithmic_ops(ctr) / max(world, 1)              # per launch (one rank's share)
-        share = {k: v / max(world, 1) for k, v in ctr.items()}
-        t_roof, binding = roof_seconds(share, sm_count, f_max)
-        achieved = ops / (t_gather * 1e-3)
-        peak_ops = ops / t_roof                                  # the pipe roof for this op mix
+        f_max = (clocks.get("sm_max_mhz") or _peaks()[0].get("sm_max_mhz", 1965.0)) * 1e6
+        share = {k: v / max(world, 1) for k, v in ctr.items()}   # one rank's launch (equal shares)
+        l2_bps = l2_bandwidth()
+        terms = roof_terms(share, sm_count, f_max, l2_bps)
+        o = pipe_ops(share)
+        ops = o["fma"] + o["alu"] + o["mufu"]
+        # headline: SM pipes + issue.  The L2 term of §8(d) counts every node / triangle byte the
+        # algorithm requests; ~92% of those requests hit L1 (profiles/), so it is reported beside the
+        # roof (frac_with_l2_requests) rather than taken as the bound.
+        core = {k: v for k, v in terms.items() if k != "l2"}
+        t_roof = max(core.values())
+        t_roof_pipes = max(v for k, v in core.items() if k != "issue")
+        binding = max(core, key=core.get)
+        t_g = t_gather * 1e-3
+        traffic, traffic_sha = measured_traffic() if args.config == 4 else (None, None)
+        cur_sha = sources_sha()
         c = ctr
         pairs, traced = c["pairs"], c["traced"]
         out = {
@@ -308,26 +353,38 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded scenegen)",
             "config": {"workload": f"C{args.config} (BASELINE.json configs[{args.config - 1}])",
                        "width": W, "height": H, "n_tris": s.n_tris, "n_lights": s.n_lights, "M": M,
-                       "K_near": r.info.get("K") if rank == 0 else None, "hit_pixels": n_hit,
+                       "K_near": r.info.get("K"), "hit_pixels": n_hit,
                        "pairs_per_step": pairs_per_step, "parallelism": f"pixel-tiles x{world}",
+                       "step": "a1-a2 scene setup + a3-a9 frame (SURVEY §8(a))",
                        "l2": "flushed between timed steps (512 MiB write)"},
-            "gather_ms": t_gather, "gather_pairs_per_s": pairs_per_step / (t_gather * 1e-3),
+            "scene_setup_ms": t["setup"], "frame_ms": t["frame"],
+            "frame_pairs_per_s": pairs_per_step / (t["frame"] * 1e-3),
+            "gather_ms": t_gather, "gather_pairs_per_s": pairs_per_step / t_g,
             "traced_fraction": traced / max(pairs, 1),
-            "traced_pairs_per_s": traced / (t_gather * 1e-3),
+            "traced_pairs_per_s": traced / t_g,
             "counters": dict(c, tri_tests_per_traced=c["tri_tests"] / max(traced, 1),
                              steps_per_packet=c["warp_steps"] / max(c["warp_rays"], 1),
                              cone_packet_fraction=c["cone_packets"] / max(c["warp_rays"], 1),
                              cache_hit_fraction=c["cache_hits"] / max(traced, 1),
                              cache_tests_per_traced=c["cache_tests"] / max(traced, 1)),
-            "roofline": {"bound": "alu", "kernel": "k_gather", "achieved": achieved / 1e12,
-                         "peak": peak_ops / 1e12, "unit": "Tops/s", "frac": achieved / peak_ops,
-                         "binding_pipe": binding, "t_roof_ms": t_roof * 1e3,
-                         "traffic": measured_traffic() if args.config == 4 else None,
-                         "traffic_unit": "bytes per launch (dram read + write, profiles/r01_gather_c4_dram.csv)",
-                         "peak_source": f"derived: {sm_count} SMs x {f_max / 1e6:.0f} MHz x measured pipe rates "
-                                        f"(FMA 128, ALU 64, MUFU 16, issue 128 thread-ops/clk/SM; "
-                                        f"profiles/r01_pipebench.jsonl), max over pipes for this op mix "
-                                        f"(DESIGN.md §5)"},
+            "roofline": {"bound": "alu", "binding_pipe": binding, "kernel": "k_gather",
+                         "achieved": ops / t_g / 1e12, "peak": ops / t_roof / 1e12, "unit": "Tops/s",
+                         "frac": t_roof / t_g, "frac_pipes_only": t_roof_pipes / t_g,
+                         "frac_with_l2_requests": max(terms.values()) / t_g,
+                         "t_roof_ms": {k: v * 1e3 for k, v in terms.items()},
+                         "ops": {k: float(v) for k, v in o.items()},
+                         "per_unit": {k: dict(zip(("fma", "alu", "mufu", "l2_bytes"), v)) for k, v in OPS.items()},
+                         "fp32_flops_per_s": 2 * o["fma"] / t_g, "fp32_peak_flops_per_s": FP32_PEAK_TFLOPS * 1e12,
+                         "fp32_note": "FMA-pipe algorithmic ops counted as FFMA (2 flop each): an upper bound",
+                         "l2_bw_bytes_per_s": l2_bps, "sm_clock_hz": f_max, "sms": sm_count,
+                         "traffic": traffic, "traffic_unit": "dram read + write bytes per launch "
+                                                             "(profiles/gather_c4_dram.csv, ncu)",
+                         "traffic_kernel_sha": traffic_sha, "kernel_sha": cur_sha,
+                         "traffic_matches_build": traffic_sha == cur_sha,
+                         "peak_source": "SURVEY §8(d) roof: per-unit algorithmic ops x counter-build counts of the "
+                                        "same kernel; pipe rates FMA 128, ALU 64, MUFU 16, issue 128 "
+                                        "thread-ops/clk/SM at the sampled max SM clock; L2 BW measured "
+                                        "(tools/pipebench.cu, profiles/r02_pipebench.jsonl)"},
             "e2e": {"value": pairs_per_step / (t_e2e * 1e-3), "unit": UNIT, "ms": t_e2e,
                     "h2d_bytes_per_step": int(s.verts.nbytes + s.albedo.nbytes),
                     "d2h_bytes_per_step": int(W * H * 3 * 4)},

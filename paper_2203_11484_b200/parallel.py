@@ -42,11 +42,52 @@ def tile_pixel_mask(W, H, tw, th, tiles):
     return m.reshape(-1)
 
 
-def assemble(rgb_local: torch.Tensor, group=None, dst=0):
-    """Framebuffer assembly: every rank holds a zero-initialised full frame
-    with only its own tiles written; a SUM reduce to `dst` is bitwise equal to
-    gathering the tiles (x + 0 = x exactly).  The reduce is in place: `dst`'s
-    buffer then holds every rank's tiles, so zero it before the next frame."""
-    import torch.distributed as dist
-    dist.reduce(rgb_local, dst, op=dist.ReduceOp.SUM, group=group)
-    return rgb_local
+class FrameAssembler:
+    """Framebuffer assembly by gather (BJ:5 "framebuffer assembled
+    with NCCL gather"): each rank packs the pixels of its own tiles (in-image
+    pixels, tile order) into a compact buffer, `dist.gather` brings the G
+    buffers to `dst`, which scatters every other rank's pixels into its frame.
+    Pure data movement (no arithmetic): `dst`'s frame equals composing the
+    tiles directly, bitwise.  Buffers are padded to the largest share (tile
+    counts differ by at most one); the pad repeats a valid pixel and is
+    dropped on unpacking.  Works on CUDA (NCCL) and CPU (gloo) tensors."""
+
+    def __init__(self, W, H, tw, th, world, device="cpu"):
+        self.world = world
+        owner = tile_owner(W, H, tw, th, world)
+        tx = (W + tw - 1) // tw
+        ys, xs = np.meshgrid(np.arange(th), np.arange(tw), indexing="ij")
+        self.idx, self.n = [], []
+        for r in range(world):
+            t = np.nonzero(owner == r)[0]
+            x = (t % tx)[:, None, None] * tw + xs[None]
+            y = (t // tx)[:, None, None] * th + ys[None]
+            ok = (x < W) & (y < H)
+            self.idx.append((y * W + x)[ok].astype(np.int64))
+            self.n.append(int(ok.sum()))
+        self.n_max = max(self.n) if self.n else 0
+        self.idx_pad = []
+        for r in range(world):
+            a = self.idx[r]
+            pad = np.full(self.n_max - len(a), a[0] if len(a) else 0, np.int64)
+            self.idx_pad.append(torch.from_numpy(np.concatenate([a, pad])).to(device))
+        self.idx = [torch.from_numpy(a).to(device) for a in self.idx]
+        self.bytes_per_rank = self.n_max * 12
+
+    def __call__(self, rgb: torch.Tensor, rank: int, group=None, dst=0):
+        import torch.distributed as dist
+        if self.world == 1:
+            return rgb
+        v = rgb.view(-1, 3)
+        send = v.index_select(0, self.idx_pad[rank])
+        # gloo gathers host tensors only (the functional multi-rank check on one GPU); NCCL gathers in HBM
+        host = dist.get_backend(group) == "gloo" and send.is_cuda
+        if host:
+            send = send.cpu()
+        recv = [torch.empty_like(send) for _ in range(self.world)] if rank == dst else None
+        dist.gather(send, recv, dst=dst, group=group)
+        if rank == dst:
+            for r in range(self.world):
+                if r != dst and self.n[r]:
+                    v.index_copy_(0, self.idx[r], recv[r][: self.n[r]].to(v.device))
+        return rgb

@@ -1,7 +1,8 @@
 """Multi-rank host logic on CPU (gloo, world_size 2 and 3): the pixel-tile
 partition covers every tile exactly once, every rank's share is balanced,
-and the framebuffer assembly (SUM reduce of zero-padded frames, §8(e)) equals
-composing the tiles directly, bitwise.  The per-tile "render" here is a
+and the framebuffer assembly (gather of each rank's packed tile pixels to
+rank 0, §8(e); the code bench.py runs under NCCL) equals composing the tiles
+directly, bitwise.  The per-tile "render" here is a
 deterministic stand-in (CPU), because the CUDA kernels need a GPU; the
 partition/assembly code is the one bench.py runs under NCCL."""
 from __future__ import annotations
@@ -15,7 +16,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2203_11484_b200.parallel import assemble, n_tiles, tile_owner, tile_pixel_mask, tiles_for_rank
+from paper_2203_11484_b200.parallel import FrameAssembler, n_tiles, tile_owner, tile_pixel_mask, tiles_for_rank
 
 
 def _free_port():
@@ -43,9 +44,12 @@ def _worker(rank, world, port, W, H, tw, th, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     tiles = tiles_for_rank(W, H, tw, th, rank, world)
     rgb = fake_render(W, H, tiles, tw, th)
+    rgb.view(-1, 3)[~torch.from_numpy(tile_pixel_mask(W, H, tw, th, tiles))] = -7.0   # other ranks' pixels: stale
     counts = torch.tensor([tiles.numel()], dtype=torch.int64)
     dist.all_reduce(counts)
-    assemble(rgb, dst=0)
+    asm = FrameAssembler(W, H, tw, th, world)
+    assert sum(asm.n) == W * H
+    asm(rgb, rank, dst=0)
     if rank == 0:
         q.put((rgb.numpy().copy(), int(counts.item())))
     dist.barrier()

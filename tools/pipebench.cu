@@ -1,5 +1,6 @@
 // pipebench.cu — issue rates of the SM pipes the gather's algorithmic ops
-// run on ("measure R_alu ... with microbenchmarks on the box").
+// run on, and the L2 read bandwidth of the node / triangle fetches (SURVEY
+// §8(d): "measure R_alu and BW_L2 with microbenchmarks on the box").
 // One CTA of 1024 threads per SM, 16 independent dependency chains per thread,
 // clock64() around the loop; prints thread-ops per clock per SM.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pipebench tools/pipebench.cu && ./pipebench
@@ -72,6 +73,49 @@ double run(int sms, float* out, long long* cyc, const char* name, int ops_per_in
     return rate;
 }
 
+// L2 read bandwidth: a 48 MB buffer (L2-resident on a 126 MB L2) read with
+// 16-byte loads that bypass L1 (ld.global.cg), every SM streaming its own
+// strided share many times; bytes / CUDA-event time.
+__global__ void k_l2(const float4* __restrict__ buf, size_t n4, int reps, float* out) {
+    float4 acc = make_float4(0, 0, 0, 0);
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (int r = 0; r < reps; ++r)
+        for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+            const float4 v = __ldcg(buf + i);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+    if (acc.x + acc.y + acc.z + acc.w == 12345.0f) out[0] = acc.x;
+}
+
+double l2_bandwidth(int sms) {
+    const size_t bytes = 48ull << 20, n4 = bytes / 16;
+    float4* buf;
+    float* out;
+    cudaMalloc(&buf, bytes);
+    cudaMalloc(&out, 4);
+    cudaMemset(buf, 0, bytes);
+    const int reps = 64;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double best = 0;
+    for (int t = 0; t < 5; ++t) {
+        k_l2<<<sms * 4, 512>>>(buf, n4, 1, out);   // warm L2
+        cudaEventRecord(e0);
+        k_l2<<<sms * 4, 512>>>(buf, n4, reps, out);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double gbs = (double)bytes * reps / (ms * 1e-3) / 1e9;
+        if (gbs > best) best = gbs;
+    }
+    printf("{\"op\": \"L2 read (ld.global.cg, 48 MB resident)\", \"GB_per_s\": %.1f}\n", best);
+    cudaFree(buf);
+    cudaFree(out);
+    return best;
+}
+
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -88,6 +132,7 @@ int main() {
     run<6>(sms, out, cyc, "MUFU.RCP", 1);
     run<7>(sms, out, cyc, "FSETP+FSEL (2 ops)", 2);
     run<8>(sms, out, cyc, "FMUL+LOP3 (1:1)", 1);
+    l2_bandwidth(sms);
     printf("{\"sm_count\": %d}\n", sms);
     return 0;
 }
