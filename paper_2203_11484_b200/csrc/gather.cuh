@@ -65,6 +65,9 @@ namespace vplgi {
 #ifndef VPL_CAND_MINRUN
 #define VPL_CAND_MINRUN 2     // shorter adaptive runs get no list (per-VPL traversal)
 #endif
+#ifndef VPL_CAND_ORDER
+#define VPL_CAND_ORDER 0      // 1: list builds push children near-to-far like beam_traverse
+#endif
 #ifndef VPL_CAND_STRADDLE
 #define VPL_CAND_STRADDLE 1   // 1: also build lists for beams with straddling axes (extent test; C4 -3%)
 #endif
@@ -135,8 +138,8 @@ __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, 
     const float tq = dot_fma(e2, q);
 #pragma unroll
     for (int k = 0; k < kGroup; ++k) {
-        if (mask & (1u << k)) {
-            if (kCount) st->tris += 1;
+        if (kGroup == 1 || (mask & (1u << k))) {   // one segment: no branch, the mask is applied below
+            if (kCount && (mask & (1u << k))) st->tris += 1;
             const f3 d = S.d[k];
             const f3 pv = cross_fma(d, e2);
             const float det = dot_fma(e1, pv);
@@ -151,6 +154,7 @@ __device__ __forceinline__ unsigned mt_segs(f3 o, const Segs& S, unsigned mask, 
             // u or v fails the other tests)
             if ((u >= 0.0f) & (v >= 0.0f) & ((u + v) <= adet) & (t > tmin * adet) & (t < S.tmax[k] * adet))
                 hit |= 1u << k;
+            hit &= mask;
         }
     }
     return hit;
@@ -471,10 +475,14 @@ int build_cands(const BvhView& bv, f3 x, bool part, const vpl_record* __restrict
 #endif
                 return -1;
             }
+#if VPL_CAND_ORDER
             const int rank = __popc(Bi & below & hmask);
             const int nh = half ? nB : nA;
             const bool rev = (dir_neg >> axis) & 1u;
             const int pos = (half ? 0 : nB) + (rev ? rank : nh - 1 - rank);
+#else
+            const int pos = __popc(Bi & below);   // collection order does not matter: push in lane order
+#endif
             if (hit && ref >= 0) sstack[sp + pos] = ref;
             sp += nA + nB;
         }
@@ -500,17 +508,17 @@ __device__ __forceinline__ void filter_cands(const BvhView& bv, f3 x, Segs& S, f
         const bool hit = ok & beam_box(B, lo, hi);
         if (kCount && lane == 0) { st->fsteps += 1; st->cones += min(32, ncand - base); }
         unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit);
-        const int ref = __float_as_int(lo.w);
+        const int toff = 3 * (~__float_as_int(lo.w) >> 3);   // float4 offset of the candidate's triangle
         while (Bl) {
-            const int k = __ffs(Bl) - 1;
-            Bl &= Bl - 1u;
-            const int tri = ~__shfl_sync(0xFFFFFFFFu, ref, k) >> 3;
-            VPL_DCHECK(tri >= 0 && tri < bv.n);
-            const float4* tr = bv.tris + 3 * tri;
+            const int k = 31 - __clz(Bl);                      // highest first: one FLO
+            Bl &= ~(1u << k);
+            const int to = __shfl_sync(0xFFFFFFFFu, toff, k);
+            VPL_DCHECK(to >= 0 && to < 3 * bv.n);
+            const float4* tr = bv.tris + to;
             const unsigned h = mt_segs<kCount>(x, S, S.pend, tmin, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), st);
             S.occ |= h;
             S.pend &= ~h;
-            if (h) cache.found(tri);
+            if (h) cache.found(to / 3);
             if (!__any_sync(0xFFFFFFFFu, S.pend != 0)) return;
         }
     }
@@ -635,7 +643,7 @@ __device__ __forceinline__ unsigned shade_group(const BvhView& bv, const vpl_rec
             const float ci = -dot_fma(xyz(nb), d);
             if (active && tri_i != tri_x && cx > 0.0f && ci > 0.0f) {
                 traced |= 1u << k;
-                w[k] = __fdividef(cx * ci, r2 * fmaxf(r2, b2));
+                w[k] = (cx * ci) * rcp_approx(r2 * fmaxf(r2, b2));   // r2 * max(r2, b2) >= b2^2: normal range
                 const float dist = sqrtf(r2);   // = sqrtf(dot(d, d)) of O9's segment setup
                 const float inv = 1.0f / dist;  // R25: dir = d * (1/dist)
                 S.d[k] = mk3(d.x * inv, d.y * inv, d.z * inv);
