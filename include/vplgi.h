@@ -166,7 +166,7 @@ VPL_API int32_t vpl_scene_consts(const void* d_scene, double* diag, float* eps, 
 
 /* -------------------------------------------------------------------- */
 /* a2  build_bvh (the paper has no acceleration structure)
- * Deterministic PLOC build (search radius 64) over the 63-bit Morton order
+ * Deterministic PLOC build (search radius VPL_PLOC_RADIUS, 128 by default, bvh.cu) over the 63-bit Morton order
  * of the centroids, SAH leaf collapse, then a 16-wide (beam traversal) and a
  * 4-wide (per-ray traversal) collapse of the same tree; boxes padded by
  * 2^-16 * max|coord| so every box test is conservative w.r.t. the exact
@@ -216,7 +216,11 @@ VPL_API int32_t vpl_render_gbuffer(const void* d_scene, const void* d_bvh, const
  * when M > 256, per-chunk partial sums: the work items are (8x4 pixel block,
  * VPL chunk) pairs, chunk = max(256, ceil(M/128) rounded up to 256), folded in
  * chunk order by the warp that completes a block's last chunk, so the image
- * depends on M only, never on the tile split). */
+ * depends on M only, never on the tile split; the partial sums live in a
+ * ring of 4096 block slots reused in block order).  Visibility of each traced
+ * pair is the exact O9 any-hit: the 16-wide BVH is culled with conservative
+ * beams (padded boxes) and, per run of 16 consecutive sorted VPLs, a list of
+ * candidate triangles gathered once with the run's beam. */
 VPL_API int32_t vpl_gather_bytes(int32_t n_vpls, int32_t width, int32_t height, size_t* work_bytes);
 VPL_API int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf,
                             const vpl_record* d_vpls, int32_t n_vpls, const int32_t* d_tiles, int32_t n_tiles,

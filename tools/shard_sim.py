@@ -3,10 +3,11 @@ pixel-tile sharding do not wait on one another (each gathers its own tiles
 with the replicated scene, BVH and VPLs), so each rank's gather can be timed
 alone, one after the other, on a single B200.  Reports, per G, every rank's
 gather time, the load-balance efficiency T(1) / (G * max_r T_r) of the
-gather, and the step efficiency once the replicated per-rank work (upload,
-BVH build, VPL generation, G-buffer of its tiles) and the collectives
-(broadcast of scene + VPLs, framebuffer reduce, at the measured 770 GB/s
-NVLink bus bandwidth of B200_PROFILING.md) are added.  This is an emulation:
+gather, the frame efficiency of SURVEY §8(e) — T = VPL generation on rank 0
++ VPL broadcast + G-buffer of the rank's tiles + gather + framebuffer gather
+(collectives at the measured 770 GB/s NVLink bus bandwidth of
+B200_PROFILING.md) — and the step efficiency with the replicated scene setup
+(upload, BVH build, scene broadcast) added, which §8(e) reports separately.  This is an emulation:
 the driver's `bench.py --gpus N` runs are the measurement.
 
   python tools/shard_sim.py --config 4 --gpus 2 4 8
@@ -51,24 +52,32 @@ def timed(fn):
     return best
 
 
-# the replicated per-rank work of one step, timed once at full size (a1-a7 without the gather)
-def pre():
+# scene setup (replicated on every rank, reported separately) and the per-frame VPL generation (rank 0)
+def setup():
     r.upload()
     r.bvh, r._bwork = V.build_bvh(r.scene, r.n, r._bvh, r._bwork)
     r._bvh = r.bvh
+
+
+def vplgen():
     r.labels, r.n_near = V.classify_near_far(r.scene, r.n, s.T)
     r.vpls, r.info, r._gwork = V.generate_vpls(r.scene, r.bvh, r.labels, r.n, s.M, s.K_near, s.max_depth, s.rr,
                                                s.seed, max_out=r.max_out, vpls=r._vbuf, work=r._gwork)
 
 
-t_pre = timed(pre)
+t_setup = timed(setup)
+t_gen = timed(vplgen)
 t_gb = timed(lambda: V.render_gbuffer(r.scene, r.bvh, r.tiles, s.width, s.height, tw, th, r.gbuf))
 t1 = timed(lambda: V.gather_indirect(r.scene, r.bvh, r.gbuf, r.vpls, r.tiles, s.width, s.height, tw, th, r.rgb))
 bw = 770e9
-coll_ms = ((s.verts.nbytes + s.albedo.nbytes + r.vpls.numel()) / bw + (s.width * s.height * 12) / bw) * 1e3
-out = {"config": s.name, "tile": [tw, th], "t1_gather_ms": t1, "replicated_ms": t_pre, "gbuffer_full_ms": t_gb,
-       "collectives_ms_est": coll_ms, "runs": []}
-step1 = t_pre + t_gb + t1
+scene_bcast_ms = (s.verts.nbytes + s.albedo.nbytes) / bw * 1e3
+vpl_bcast_ms = r.vpls.numel() / bw * 1e3
+fb_ms = (s.width * s.height * 12) / bw * 1e3           # every pixel crosses NVLink once into rank 0
+out = {"config": s.name, "tile": [tw, th], "t1_gather_ms": t1, "scene_setup_ms": t_setup, "vplgen_ms": t_gen,
+       "gbuffer_full_ms": t_gb, "scene_bcast_ms_est": scene_bcast_ms, "vpl_bcast_ms_est": vpl_bcast_ms,
+       "fb_gather_ms_est": fb_ms, "runs": []}
+frame1 = t_gen + t_gb + t1
+step1 = t_setup + frame1
 for G in a.gpus:
     tr = []
     for rank in range(G):
@@ -76,7 +85,9 @@ for G in a.gpus:
         tr.append(timed(lambda: V.gather_indirect(r.scene, r.bvh, r.gbuf, r.vpls, tiles, s.width, s.height, tw, th,
                                                   r.rgb)))
     tmax = max(tr)
-    stepG = t_pre + t_gb / G + tmax + coll_ms
+    frameG = t_gen + vpl_bcast_ms + t_gb / G + tmax + fb_ms
+    stepG = t_setup + scene_bcast_ms + frameG
     out["runs"].append({"G": G, "rank_gather_ms": tr, "gather_efficiency": t1 / (G * tmax),
+                        "frame_ms_est": frameG, "frame_efficiency_est": frame1 / (G * frameG),
                         "step_ms_est": stepG, "step_efficiency_est": step1 / (G * stepG)})
 print(json.dumps(out), flush=True)
