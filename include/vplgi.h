@@ -133,6 +133,8 @@ typedef struct {
     unsigned long long cand_fails;   /* clusters whose list could not be used (loose beam or overflow) */
     unsigned long long filter_steps; /* per-VPL candidate-filter iterations (32 candidates each) */
     unsigned long long cand_steps;   /* traversal steps spent building the lists (part of warp_steps) */
+    unsigned long long filter_mt;    /* warp-level MT tests issued by the list filter */
+    unsigned long long filter_mt_hits; /* ... of which found an occluder for some lane */
 } vpl_counters;
 
 /* -------------------------------------------------------------------- */

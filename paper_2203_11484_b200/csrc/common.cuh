@@ -133,6 +133,7 @@ struct BvhView {
     const float4* wide4;   // 4-wide nodes (per-ray packet traversal)
     int32_t root;
     int32_t n;             // triangles (bounds checks under VPL_DEBUG)
+    float box_pad;         // the scene's box padding (SceneHdr::box_pad), set by callers that need it
 };
 inline size_t bvh_layout(int64_t n, BvhHdr* h) {
     size_t off = align_up(sizeof(BvhHdr));
@@ -157,6 +158,7 @@ inline BvhView bvh_view(const void* blob, int64_t n) {
     v.wide4 = (const float4*)((const char*)blob + h.off_wide4);
     v.root = h.root;
     v.n = (int32_t)n;
+    v.box_pad = 0.0f;
     return v;
 }
 
@@ -308,6 +310,8 @@ struct TravStats {
     uint32_t lists = 0, entries = 0, lfail = 0;       // cluster candidate lists built / their entries / unusable
     uint32_t fsteps = 0;                              // candidate-filter iterations (32 candidates each)
     uint32_t lsteps = 0;                              // traversal steps spent building candidate lists
+    uint32_t ftests = 0;                              // frustum pre-tests of list triangles (lane-level)
+    uint32_t fmt = 0, fmt_hit = 0;                    // filter MT tests (warp-level) / those with a hit
 };
 
 // leaf refs: ~((first << 3) | (count - 1)), count in [1, 8]

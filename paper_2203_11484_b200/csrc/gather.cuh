@@ -65,6 +65,12 @@ namespace vplgi {
 #ifndef VPL_CAND_MINRUN
 #define VPL_CAND_MINRUN 2     // shorter adaptive runs get no list (per-VPL traversal)
 #endif
+#ifndef VPL_SCAP
+#define VPL_SCAP 0.5f   // beam s-range cap at each end, in units of eps / |D|max (O9 tests t in (eps, L - eps))
+#endif
+#ifndef VPL_CAND_HYBRID
+#define VPL_CAND_HYBRID 0     // 1: a list that would overflow keeps its unexpanded subtrees as entries (C4 +15%, off)
+#endif
 #ifndef VPL_CAND_ORDER
 #define VPL_CAND_ORDER 0      // 1: list builds push children near-to-far like beam_traverse
 #endif
@@ -231,7 +237,7 @@ __device__ __forceinline__ bool beam_from_bounds(const float* Dn, const float* D
     }
     // segment (x_j, y_k) tests t in (eps, L - eps): s = 1 - t/L in (eps/L, 1 - eps/L) within
     // [eps/Lmax, 1 - eps/Lmax]; half the cap is cut (the rest is slack for MT's rounding of t)
-    B.s_lo = (0.5f * eps) * rcp_approx(lmax);   // relative error ~1e-6: far inside the factor 1/2
+    B.s_lo = (VPL_SCAP * eps) * rcp_approx(lmax);   // relative error ~1e-6: far inside the factor
     B.s_hi = 1.0f - B.s_lo;
     return tight;
 }
@@ -288,7 +294,7 @@ __device__ __forceinline__ bool cluster_beam_box(const ClusterBeam& C, float4 lo
 template <bool kCount>
 __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, float tmin, const Beam& B,
                                               unsigned dir_neg, OccluderCache& cache, int* __restrict__ sstack,
-                                              TravStats* st) {
+                                              TravStats* st, int sp0 = 0) {
     const int lane = threadIdx.x & 31;
     const int half = lane >> 4;
     const unsigned below = (1u << lane) - 1u;
@@ -297,10 +303,13 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
         test_tri<kCount>(bv, x, S, tmin, 0, cache, st);
         return;
     }
-    // the stack holds inner nodes only
-    if (lane == 0) sstack[0] = bv.root;
-    __syncwarp();
-    int sp = 1;
+    // the stack holds inner nodes only; sp0 > 0: the caller pre-filled it (a hybrid list's subtrees)
+    int sp = sp0;
+    if (sp0 == 0) {
+        if (lane == 0) sstack[0] = bv.root;
+        __syncwarp();
+        sp = 1;
+    }
 #if VPL_SMEM_ADDR
     const unsigned sbase = (unsigned)__cvta_generic_to_shared(sstack);   // 32-bit shared-window address
 #endif
@@ -346,7 +355,7 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, f3 x, Segs& S, 
             if (hit && ref >= 0) sstack[sp + pos] = ref;
 #endif
             sp += nA + nB;
-            VPL_DCHECK(sp <= kWarpStack);
+            VPL_DCHECK(sp <= kWarpStack - kCandCap);   // a live candidate list occupies the top kCandCap
         }
         __syncwarp();
         while (Bl) {   // hit triangle children
@@ -432,8 +441,10 @@ int build_cands(const BvhView& bv, f3 x, bool part, const vpl_record* __restrict
     if (!make_cluster_beam(xl, xh, ylo, yhi, eps, CB)) return -1;
     const int half = lane >> 4;
     const unsigned below = (1u << lane) - 1u;
+#if VPL_CAND_ORDER
     const unsigned hmask = half ? 0xFFFF0000u : 0x0000FFFFu;
     const unsigned dir_neg = CB.B.pos;
+#endif
     if (lane == 0) sstack[0] = bv.root;
     __syncwarp();
     int sp = 1, n = 0;
@@ -447,7 +458,9 @@ int build_cands(const BvhView& bv, f3 x, bool part, const vpl_record* __restrict
         const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)slot << 5));
         const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
         const int ref = node >= 0 ? __float_as_int(lo.w) : INT_MIN;
+#if VPL_CAND_ORDER
         const int axis = __float_as_int(hi.w);
+#endif
         const bool hit = (ref != INT_MIN) & cluster_beam_box(CB, lo, hi);
         if (kCount) {
             const unsigned real = __ballot_sync(0xFFFFFFFFu, ref != INT_MIN);
@@ -455,26 +468,47 @@ int build_cands(const BvhView& bv, f3 x, bool part, const vpl_record* __restrict
         }
         const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
         const unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
+        const int nl = __popc(Bl), ni = __popc(Bi);
+#if VPL_CAND_HYBRID
+        // invariant n + sp <= kCandCap: if this step's results would break it, the two nodes just
+        // popped and every node still on the stack go into the list unexpanded (node | 0x80000000):
+        // each VPL then tests the expanded part flat and traverses those subtrees with its own beam
+        if (n + nl + sp + ni > kCandCap) {
+            __syncwarp();
+            const unsigned Bp = __ballot_sync(0xFFFFFFFFu, (lane & (kWide - 1)) == 0 && node >= 0);
+            if ((lane & (kWide - 1)) == 0 && node >= 0)
+                sstack[kWarpStack - 1 - (n + __popc(Bp & below))] = node | (int)0x80000000u;
+            n += __popc(Bp);
+            for (int k = lane; k < sp; k += 32) sstack[kWarpStack - 1 - (n + k)] = sstack[k] | (int)0x80000000u;
+            n += sp;
+            __syncwarp();
+            if (kCount && lane == 0) st->lfail += 1;   // counted as a partial list
+            return n;
+        }
+#endif
         __syncwarp();
         if (Bl) {
-            const int nl = __popc(Bl);
+#if !VPL_CAND_HYBRID
             if (n + nl > kCandCap) {
 #ifdef VPL_CAND_DIAG
                 if (kCount && lane == 0) st->boxes += 1u << 20;   // diagnostic builds: overflow count in box_tests
 #endif
                 return -1;
             }
+#endif
             if (hit && ref < 0) sstack[kWarpStack - 1 - (n + __popc(Bl & below))] = slot;
             n += nl;
         }
         if (Bi) {
             const int nB = __popc(Bi >> 16), nA = __popc(Bi & 0xFFFFu);
+#if !VPL_CAND_HYBRID
             if (sp + nA + nB > kWarpStack - kCandCap) {
 #ifdef VPL_CAND_DIAG
                 if (kCount && lane == 0) st->boxes += 1u << 20;
 #endif
                 return -1;
             }
+#endif
 #if VPL_CAND_ORDER
             const int rank = __popc(Bi & below & hmask);
             const int nh = half ? nB : nA;
@@ -491,22 +525,114 @@ int build_cands(const BvhView& bv, f3 x, bool part, const vpl_record* __restrict
     return n;
 }
 
+// Frustum of one VPL's pending segments (apex y, the VPL): with m the dominant axis of the first
+// pending segment's direction d_j = (y - x_j)/L_j and a, b the other two, every pending d_j has the
+// same sign of d_m (a tight beam never changes sign) and slopes p_j = d_a/d_m, q_j = d_b/d_m; every
+// point of segment j is P = y - s L_j d_j, s in [0, 1], so with sigma = -sign(d_m),
+// A = sigma (P - y)_a, B = sigma (P - y)_b, U = sigma (P - y)_m it satisfies U >= 0,
+// pmin U <= A <= pmax U, qmin U <= B <= qmax U (slopes
+// widened by 2^-18 relative).  A triangle whose three vertices all violate one of these by more than
+// the margin (the box padding, times the plane normal's L1 norm) cannot be crossed by any pending
+// segment: the same conservative argument as the padded boxes (MT's rounding stays far inside it).
+#ifndef VPL_FRUSTUM
+#define VPL_FRUSTUM 0   // 1: frustum pre-test before MT in the filter (C4: filter MT -19%, time +8%; off)
+#endif
+struct Frustum {
+    int a, b, m;
+    float sg, yA, yB, yU;           // sigma and the apex in the (A, B, U) frame
+    float pmin, pmax, qmin, qmax;
+    float mp, mq, mu;               // margins
+    __device__ __forceinline__ void make(const Segs& S, f3 y, float pad) {
+        const float inf = __int_as_float(0x7f800000);
+        const bool live = S.pend != 0;
+        const unsigned act = __ballot_sync(0xFFFFFFFFu, live);
+        const int l0 = __ffs(act) - 1;
+        const f3 d = S.d[0];
+        const float ax = fabsf(d.x), ay = fabsf(d.y), az = fabsf(d.z);
+        const int mm = (ax >= ay && ax >= az) ? 0 : (ay >= az ? 1 : 2);
+        m = __shfl_sync(0xFFFFFFFFu, mm, l0);
+        a = m == 0 ? 1 : 0;
+        b = m == 2 ? 1 : 2;
+        const float dv[3] = {d.x, d.y, d.z};
+        const float dm = dv[m], da = dv[a], db = dv[b];
+        const float r = __fdividef(1.0f, dm);
+        const float p = live ? da * r : 0.0f, q = live ? db * r : 0.0f;
+        sg = __shfl_sync(0xFFFFFFFFu, dm, l0) < 0.0f ? 1.0f : -1.0f;   // P - y = -s L d_j: U = sigma (P - y)_m >= 0
+        const float p0 = warp_min_f32(live ? p : inf), p1 = warp_max_f32(live ? p : -inf);
+        const float q0 = warp_min_f32(live ? q : inf), q1 = warp_max_f32(live ? q : -inf);
+        const float w = 0x1p-18f;
+        pmin = p0 - w * (fabsf(p0) + 1.0f); pmax = p1 + w * (fabsf(p1) + 1.0f);
+        qmin = q0 - w * (fabsf(q0) + 1.0f); qmax = q1 + w * (fabsf(q1) + 1.0f);
+        const float yv[3] = {y.x, y.y, y.z};
+        yA = sg * yv[a]; yB = sg * yv[b]; yU = sg * yv[m];
+        mp = pad * (1.0f + fmaxf(fabsf(pmin), fabsf(pmax)));
+        mq = pad * (1.0f + fmaxf(fabsf(qmin), fabsf(qmax)));
+        mu = pad;
+    }
+    // v0 = a.xyz, v1 = v0 + e1, v2 = v0 + e2 (the leaf-ordered triangle record)
+    __device__ __forceinline__ bool culls(float4 t0, float4 t1, float4 t2) const {
+        const float v0[3] = {t0.x, t0.y, t0.z};
+        const float e1[3] = {t1.x, t1.y, t1.z}, e2[3] = {t2.x, t2.y, t2.z};
+        float A[3], B[3], U[3];
+        const float s = sg;
+        A[0] = s * v0[a] - yA; A[1] = s * (v0[a] + e1[a]) - yA; A[2] = s * (v0[a] + e2[a]) - yA;
+        B[0] = s * v0[b] - yB; B[1] = s * (v0[b] + e1[b]) - yB; B[2] = s * (v0[b] + e2[b]) - yB;
+        U[0] = s * v0[m] - yU; U[1] = s * (v0[m] + e1[m]) - yU; U[2] = s * (v0[m] + e2[m]) - yU;
+        // each plane: cull iff min over the vertices of its outside distance > margin
+        const float f1 = fmin3(fmaf(-pmax, U[0], A[0]), fmaf(-pmax, U[1], A[1]), fmaf(-pmax, U[2], A[2]));
+        const float f2 = fmin3(fmaf(pmin, U[0], -A[0]), fmaf(pmin, U[1], -A[1]), fmaf(pmin, U[2], -A[2]));
+        const float f3v = fmin3(fmaf(-qmax, U[0], B[0]), fmaf(-qmax, U[1], B[1]), fmaf(-qmax, U[2], B[2]));
+        const float f4 = fmin3(fmaf(qmin, U[0], -B[0]), fmaf(qmin, U[1], -B[1]), fmaf(qmin, U[2], -B[2]));
+        const float f5 = -fmax3(U[0], U[1], U[2]);
+        return (f1 > mp) | (f2 > mp) | (f3v > mq) | (f4 > mq) | (f5 > mu);
+    }
+};
+
 // The pending segments of one VPL against its cluster's candidate list: lane c
 // tests candidate c of each batch of 32 against the VPL's own beam; hit
 // triangles get the exact MT of O9 from every lane with a pending segment.
 template <bool kCount>
 __device__ __forceinline__ void filter_cands(const BvhView& bv, f3 x, Segs& S, float tmin, const Beam& B,
-                                             const int* __restrict__ sstack, int ncand, OccluderCache& cache,
-                                             TravStats* st) {
+                                             int* __restrict__ sstack, int ncand, OccluderCache& cache,
+                                             TravStats* st, f3 y) {
     const int lane = threadIdx.x & 31;
+#if VPL_CAND_HYBRID
+    const unsigned below = (1u << lane) - 1u;
+#endif
+#if VPL_FRUSTUM
+    Frustum F;
+    F.make(S, y, fmaxf(bv.box_pad, tmin));
+#endif
+#if VPL_CAND_HYBRID
+    int sp = 0;   // subtrees of a hybrid list, traversed after the flat part
+#endif
     for (int base = 0; base < ncand; base += 32) {
         const int i = base + lane;
         const bool ok = i < ncand;
-        const int slot = ok ? sstack[kWarpStack - 1 - i] : 0;   // slot 0: a real child, masked below
+        const int e = ok ? sstack[kWarpStack - 1 - i] : 0;     // child slot, or node | 0x80000000
+        const bool sub = e < 0;
+        const int slot = sub ? 0 : e;                          // slot 0: a real child, masked below
         const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)slot << 5));
         const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
-        const bool hit = ok & beam_box(B, lo, hi);
+        bool hit = ok & !sub & beam_box(B, lo, hi);
         if (kCount && lane == 0) { st->fsteps += 1; st->cones += min(32, ncand - base); }
+#if VPL_FRUSTUM
+        if (__any_sync(0xFFFFFFFFu, hit)) {   // frustum pre-test of the box hits (lane-parallel)
+            const int to0 = 3 * (~__float_as_int(lo.w) >> 3);
+            const float4* tr = bv.tris + (hit ? to0 : 0);
+            const float4 a = __ldg(tr), b = __ldg(tr + 1), c = __ldg(tr + 2);
+            if (kCount && hit) st->ftests += 1;
+            hit &= !F.culls(a, b, c);
+        }
+#endif
+#if VPL_CAND_HYBRID
+        const unsigned Bs = __ballot_sync(0xFFFFFFFFu, ok && sub);
+        if (Bs) {
+            if (ok && sub) sstack[sp + __popc(Bs & below)] = e & 0x7FFFFFFF;
+            sp += __popc(Bs);
+            __syncwarp();
+        }
+#endif
         unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit);
         const int toff = 3 * (~__float_as_int(lo.w) >> 3);   // float4 offset of the candidate's triangle
         while (Bl) {
@@ -516,12 +642,19 @@ __device__ __forceinline__ void filter_cands(const BvhView& bv, f3 x, Segs& S, f
             VPL_DCHECK(to >= 0 && to < 3 * bv.n);
             const float4* tr = bv.tris + to;
             const unsigned h = mt_segs<kCount>(x, S, S.pend, tmin, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), st);
+            if (kCount) {   // warp-level MT tests of the filter, and those that found an occluder
+                const bool any = __any_sync(0xFFFFFFFFu, h != 0);
+                if (lane == 0) { st->fmt += 1; st->fmt_hit += any; }
+            }
             S.occ |= h;
             S.pend &= ~h;
             if (h) cache.found(to / 3);
             if (!__any_sync(0xFFFFFFFFu, S.pend != 0)) return;
         }
     }
+#if VPL_CAND_HYBRID
+    if (sp > 0) beam_traverse<kCount>(bv, x, S, tmin, B, B.pos, cache, sstack, st, sp);
+#endif
 }
 
 // Resolve the pending segments of a group: beam over the group, else one beam
@@ -551,7 +684,7 @@ __device__ __forceinline__ void resolve_group(const BvhView& bv, f3 x, Segs& S, 
         // the list covers the participating receivers only (the cluster cull is conservative, so a lane
         // with a pending segment always participates; checked anyway)
         if (VPL_CANDS && kGroup == 1 && cand >= 0 && !__any_sync(0xFFFFFFFFu, S.pend && !part))
-            filter_cands<kCount>(bv, x, S, eps, B, sstack, cand, cache, st);
+            filter_cands<kCount>(bv, x, S, eps, B, sstack, cand, cache, st, yk[0]);
         else
             beam_traverse<kCount>(bv, x, S, eps, B, B.pos, cache, sstack, st);
     } else {

@@ -249,11 +249,11 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
         }
         if (kCount) {
             unsigned long long pairs = active ? (unsigned long long)(vend - vbeg) : 0ull;
-            unsigned long long v[17] = {pairs, n_traced, n_vis, st.boxes, st.tris, st.wrays, st.wsteps,
+            unsigned long long v[19] = {pairs, n_traced, n_vis, st.boxes, st.tris, st.wrays, st.wsteps,
                                         st.cones, st.cpk, st.rpk, st.chits, st.ctests, st.lists, st.entries,
-                                        st.lfail, st.fsteps, st.lsteps};
+                                        st.lfail, st.fsteps, st.lsteps, st.fmt, st.fmt_hit};
 #pragma unroll
-            for (int q = 0; q < 17; ++q) {
+            for (int q = 0; q < 19; ++q) {
                 unsigned long long a = v[q];
                 for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
                 if (lane == 0) atomicAdd(&ctr->pairs + q, a);
@@ -625,6 +625,7 @@ static int32_t gather_impl(const void* d_scene, const void* d_bvh, const vpl_gpo
     int grid = sms * VPL_GATHER_CTAS;  // persistent: VPL_GATHER_CTAS one-warp CTAs per SM
     SceneView sv = scene_view(d_scene, hh.n);
     BvhView bv = bvh_view(d_bvh, hh.n);
+    bv.box_pad = hh.box_pad;
 #ifdef VPL_CARVEOUT
     // shared-memory carveout preference (percent of the unified L1/shared array; tuning builds only)
     VPL_CUDA(cudaFuncSetAttribute(k_gather<false>, cudaFuncAttributePreferredSharedMemoryCarveout, VPL_CARVEOUT));

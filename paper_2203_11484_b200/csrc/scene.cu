@@ -1,6 +1,9 @@
 // scene.cu — a1 scene_upload (O1) and a3 classify_near_far (O2).
 #include "common.cuh"
 
+#ifndef VPL_BOX_PAD
+#define VPL_BOX_PAD 0x1p-16f   // BVH box padding relative to max |coordinate|
+#endif
 namespace vplgi {
 
 __device__ __forceinline__ uint32_t fenc(float f) {
@@ -79,10 +82,11 @@ __global__ void k_scene_consts(SceneHdr* h, int64_t* d_bad) {
     h->diag = diag;
     h->eps = (float)(1e-4 * diag);
     h->b2 = (float)((0.01 * diag) * (0.01 * diag));
-    h->box_pad = m * 0x1p-16f;  // conservative BVH box padding
+    h->box_pad = m * VPL_BOX_PAD;  // conservative BVH box padding
     if (d_bad) *d_bad = h->bad == ~0ull ? -1 : (int64_t)h->bad;
 }
 
+// (knob definitions must precede use; see the top of this file)
 // O2 — near iff the centroid is strictly inside the frustum and closer than T
 __global__ void k_classify(const SceneHdr* __restrict__ h, const float4* __restrict__ cen, int64_t n, float T2,
                            uint8_t* __restrict__ labels, unsigned long long* __restrict__ n_near) {
