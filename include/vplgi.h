@@ -63,7 +63,13 @@ enum {
 /* Area light (BJ:7-11 use 0.5 x 0.5 m quads; R2): the parallelogram
  * corner + a*e_u + b*e_v (a, b in [0,1]) emitting radiance `radiance` on the
  * side of `normal`; `area` = |e_u x e_v|.  16 floats, the row layout of
- * scenegen's light array. */
+ * scenegen's light array.
+ * Point light (Eq. 2's literal form P:51-56; reading R27):
+ * area == 0 marks an isotropic point light at `corner` (e_u = e_v = 0,
+ * `normal` ignored) whose `radiance` field holds its power Phi (W per
+ * channel): near VPLs get Phi cos(omega)/(4 pi r^2) V per unit represented
+ * area (times rho/pi), walks start with power Phi n_L in a uniform
+ * direction on the sphere, and the direct term needs no light samples. */
 typedef struct {
     float corner[3], e_u[3], e_v[3], normal[3], area, radiance[3];
 } vpl_light;

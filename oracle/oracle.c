@@ -378,6 +378,18 @@ static inline f3 light_corner(const float* L) { return ld3(L); }
 static inline f3 light_eu(const float* L) { return ld3(L + 3); }
 static inline f3 light_ev(const float* L) { return ld3(L + 6); }
 static inline f3 light_n(const float* L) { return ld3(L + 9); }
+/* Point lights (reading R27, "the light sources are all point lights",
+ * Eq. 2's literal form P:51-56): a light row with area == 0 is an isotropic
+ * point light at `corner` (e_u = e_v = 0) whose `radiance` field holds its
+ * power Phi (W per channel, R3).  It has no facing side. */
+static inline int light_is_point(const float* L) { return L[12] == 0.0f; }
+/* Eq. 2's geometry term for a point light without D (R1: omega_i and r
+ * relative to the light): cos(omega) / (4 pi r^2) = cp / ((r2 * sqrt(r2)) * 4pi),
+ * cp = n.d (unnormalised d = light - x, so cos(omega) = cp / r). */
+static inline float point_g(float cp, float r2) {
+    const float FOUR_PI = (float)(4.0 * PI_D);
+    return cp / ((r2 * sqrtf(r2)) * FOUR_PI);
+}
 /* light centre = (corner + 0.5*e_u) + 0.5*e_v (O3) */
 static inline f3 light_centre(const float* L) {
     return add(add(light_corner(L), scl(0.5f, light_eu(L))), scl(0.5f, light_ev(L)));
@@ -394,7 +406,8 @@ void oracle_lit(const OScene* s, const uint8_t* labels, uint8_t* lit) {
         for (int l = 0; l < s->nL; l++) {
             const float* L = s->lights + 16 * l;
             f3 cl = light_centre(L);
-            if (dot(n, sub(cl, c)) > 0.0f && dot(light_n(L), sub(c, cl)) > 0.0f && !occluded(s, c, cl)) {
+            if (dot(n, sub(cl, c)) > 0.0f && (light_is_point(L) || dot(light_n(L), sub(c, cl)) > 0.0f) &&
+                !occluded(s, c, cl)) {
                 lit[i] = 1;
                 break;
             }
@@ -515,6 +528,13 @@ static void near_vpl(const OScene* s, const OParams* p, const int64_t* order, co
         f3 d = sub(y, x);
         float r2 = dot(d, d);
         float cp = dot(n, d);
+        if (light_is_point(L)) { /* R27: Phi * cos(omega) / (4 pi r^2) * V */
+            if (cp > 0.0f && !occluded(s, x, y)) {
+                float g = point_g(cp, r2);
+                for (int c = 0; c < 3; c++) E[c] += L[13 + c] * g;
+            }
+            continue;
+        }
         float cl = -dot(light_n(L), d);
         if (cp > 0.0f && cl > 0.0f && !occluded(s, x, y)) {
             float g = ((L[12] * cp) * cl) / (r2 * r2);
@@ -551,6 +571,21 @@ static f3 malley(const OScene* s, uint64_t seed, uint32_t w, uint32_t* j, f3 n) 
     return mk((a * t1.x + b * t2.x) + z * n.x, (a * t1.y + b * t2.y) + z * n.y, (a * t1.z + b * t2.z) + z * n.z);
 }
 
+/* Uniform direction on the sphere for a point light's emission (R27), with
+ * no transcendental: rejection in the cube, a,b,c = 2U - 1 until
+ * 0 < a*a + b*b + c*c <= 1 (at most 64 attempts, else (0, 0, 1)); the
+ * direction (a, b, c) is not normalised (MT and x = o + t*dir do not need it). */
+static f3 sphere_dir(uint64_t seed, uint32_t w, uint32_t* j) {
+    for (int att = 0; att < 64; att++) {
+        float a = 2.0f * u01(oracle_draw(seed, STREAM_WALK, w, (*j)++)) - 1.0f;
+        float b = 2.0f * u01(oracle_draw(seed, STREAM_WALK, w, (*j)++)) - 1.0f;
+        float c = 2.0f * u01(oracle_draw(seed, STREAM_WALK, w, (*j)++)) - 1.0f;
+        float q = (a * a + b * b) + c * c;
+        if (q > 0.0f && q <= 1.0f) return mk(a, b, c);
+    }
+    return mk(0.0f, 0.0f, 1.0f);
+}
+
 /* O10 — one sparse-IR walk (P:15, P:35, P:46 step 3; R9-R11).  Writes up to
  * max_depth deposits (flux not yet divided by the walk count); returns count. */
 static int walk(const OScene* s, const OParams* p, const uint8_t* labels, uint32_t w, OVpl* dep) {
@@ -559,11 +594,14 @@ static int walk(const OScene* s, const OParams* p, const uint8_t* labels, uint32
     int l = (int)(((uint64_t)x0 * (uint64_t)s->nL) >> 32);
     const float* L = s->lights + 16 * l;
     float beta[3];
-    for (int c = 0; c < 3; c++) beta[c] = (float)(PI_D * (double)L[12] * (double)L[13 + c] * (double)s->nL);
+    /* beta0 = power of light l x n_L: pi A L for an area light, Phi for a point light (R27) */
+    for (int c = 0; c < 3; c++)
+        beta[c] = light_is_point(L) ? (float)((double)L[13 + c] * (double)s->nL)
+                                    : (float)(PI_D * (double)L[12] * (double)L[13 + c] * (double)s->nL);
     float u1 = u01(oracle_draw(p->seed, STREAM_WALK, w, j++));
     float u2 = u01(oracle_draw(p->seed, STREAM_WALK, w, j++));
-    f3 o = add(add(light_corner(L), scl(u1, light_eu(L))), scl(u2, light_ev(L)));
-    f3 dir = malley(s, p->seed, w, &j, light_n(L));
+    f3 o = add(add(light_corner(L), scl(u1, light_eu(L))), scl(u2, light_ev(L)));   /* point: e_u = e_v = 0 */
+    f3 dir = light_is_point(L) ? sphere_dir(p->seed, w, &j) : malley(s, p->seed, w, &j, light_n(L));
     const float INV_PI = (float)(1.0 / PI_D);
     int cnt = 0;
     for (int d = 1; d <= p->max_depth; d++) {
@@ -781,7 +819,9 @@ void oracle_gather(const OScene* s, const OGbuf* gb, int64_t n_pix, const OVpl* 
 /*   E_c += L_l,c * ((A_l * cx) * cl) / (r2 * r2)  if cx > 0, cl > 0, V(x,y), */
 /* d = y - x, cx = n_x.d, cl = -n_l.d (the same form as O8), draws 2(lS+s)  */
 /* and 2(lS+s)+1 of Philox stream 4, item = pixel index; fp32 in this order. */
-/* out_c = (rho_c * (E_c * inv_S)) * INV_PI; miss / back face -> 0.          */
+/* out_c = (rho_c * (E_c * inv_S + P_c)) * INV_PI; miss / back face -> 0.    */
+/* A point light (R27) needs no samples: P_c += Phi_c * cx / ((r2 sqrt r2)  */
+/* 4 pi) if cx > 0 and V(x, y) (the same term as O8's point form).          */
 /* ------------------------------------------------------------------------ */
 void oracle_direct(const OScene* s, const OGbuf* gb, const int32_t* pix, int64_t n_pix, int32_t S, uint64_t seed,
                    float inv_S, float* rgb) {
@@ -789,12 +829,23 @@ void oracle_direct(const OScene* s, const OGbuf* gb, const int32_t* pix, int64_t
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t k = 0; k < n_pix; k++) {
         const OGbuf* g = gb + k;
-        float E[3] = {0.0f, 0.0f, 0.0f};
+        float E[3] = {0.0f, 0.0f, 0.0f}, Pt[3] = {0.0f, 0.0f, 0.0f};
         int ok = g->tri >= 0 && g->front;
         if (ok) {
             f3 x = ld3(g->pos), nx = ld3(g->nrm);
             for (int l = 0; l < s->nL; l++) {
                 const float* L = s->lights + 16 * l;
+                if (light_is_point(L)) {
+                    f3 y = light_corner(L);
+                    f3 d = sub(y, x);
+                    float r2 = dot(d, d);
+                    float cx = dot(nx, d);
+                    if (cx > 0.0f && !occluded(s, x, y)) {
+                        float gg = point_g(cx, r2);
+                        for (int c = 0; c < 3; c++) Pt[c] += L[13 + c] * gg;
+                    }
+                    continue;
+                }
                 for (int q = 0; q < S; q++) {
                     uint32_t j = 2u * (uint32_t)(l * S + q);
                     float u = u01(oracle_draw(seed, STREAM_DIRECT, (uint32_t)pix[k], j));
@@ -811,7 +862,7 @@ void oracle_direct(const OScene* s, const OGbuf* gb, const int32_t* pix, int64_t
                 }
             }
         }
-        for (int c = 0; c < 3; c++) rgb[3 * k + c] = ok ? (g->alb[c] * (E[c] * inv_S)) * INV_PI : 0.0f;
+        for (int c = 0; c < 3; c++) rgb[3 * k + c] = ok ? (g->alb[c] * ((E[c] * inv_S) + Pt[c])) * INV_PI : 0.0f;
     }
 }
 

@@ -194,6 +194,17 @@ __device__ __forceinline__ f3 cross(f3 a, f3 b) {
     return f3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
 
+// ------------------------------------------------------------------ lights
+// A light row (vpl_light, 16 floats) with area == 0 is an isotropic point light at `corner` whose
+// `radiance` field holds its power Phi (reading R27; e_u = e_v = 0).
+__device__ __forceinline__ bool light_is_point(const float* L) { return L[12] == 0.0f; }
+// Eq. 2's point-light geometry term without D (R1): cos(omega) / (4 pi r^2) with
+// cos(omega) = cp / r, cp = n.d for the unnormalised d = light - x: cp / ((r2 sqrt(r2)) 4 pi), exact fp32
+__device__ __forceinline__ float point_g(float cp, float r2) {
+    constexpr float kFourPi = (float)(4.0 * 3.14159265358979323846);
+    return cp / ((r2 * sqrtf(r2)) * kFourPi);
+}
+
 // ------------------------------------------------------------------ Philox4x32-10
 struct Philox {
     // counter = (j >> 2, item, stream, 0), key = (seed lo, seed hi); draw j = lane j & 3

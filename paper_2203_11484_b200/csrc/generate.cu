@@ -42,7 +42,7 @@ __global__ void k_lit(SceneView sv, BvhView bv, const uint8_t* __restrict__ labe
         for (int l = 0; l < h->nL && !r; ++l) {
             const float* L = h->lights + 16 * l;
             f3 cl = (light_corner(L) + 0.5f * light_eu(L)) + 0.5f * light_ev(L);
-            if (dot(nn, cl - c) > 0.0f && dot(light_n(L), c - cl) > 0.0f &&
+            if (dot(nn, cl - c) > 0.0f && (light_is_point(L) || dot(light_n(L), c - cl) > 0.0f) &&
                 !segment_occluded<false>(bv, c, cl, eps, nullptr))
                 r = 1;
         }
@@ -158,6 +158,15 @@ __global__ void k_strata(SceneView sv, BvhView bv, const int32_t* __restrict__ o
         f3 d = y - p;
         float r2 = dot(d, d);
         float cp = dot(nn, d);
+        if (light_is_point(L)) {   // R27: Eq. 2's point form, Phi cos(omega) / (4 pi r^2) V
+            if (cp > 0.0f && !segment_occluded<false>(bv, p, y, eps, nullptr)) {
+                float g = point_g(cp, r2);
+                E[0] += L[13] * g;
+                E[1] += L[14] * g;
+                E[2] += L[15] * g;
+            }
+            continue;
+        }
         float cl = -dot(light_n(L), d);
         if (cp > 0.0f && cl > 0.0f && !segment_occluded<false>(bv, p, y, eps, nullptr)) {
             float g = ((L[12] * cp) * cl) / (r2 * r2);
@@ -202,6 +211,19 @@ __device__ __forceinline__ f3 malley(Philox& rng, f3 n) {
     return mk3((a * t1.x + b * t2.x) + z * n.x, (a * t1.y + b * t2.y) + z * n.y, (a * t1.z + b * t2.z) + z * n.z);
 }
 
+// Uniform direction on the sphere for a point light's emission (R27): rejection in the cube,
+// a, b, c = 2U - 1 until 0 < a*a + b*b + c*c <= 1 (<= 64 attempts, else (0, 0, 1)); not normalised
+__device__ __forceinline__ f3 sphere_dir(Philox& rng) {
+    for (int att = 0; att < 64; ++att) {
+        float a = 2.0f * u01(rng.next()) - 1.0f;
+        float b = 2.0f * u01(rng.next()) - 1.0f;
+        float c = 2.0f * u01(rng.next()) - 1.0f;
+        float q = (a * a + b * b) + c * c;
+        if (q > 0.0f && q <= 1.0f) return mk3(a, b, c);
+    }
+    return mk3(0.0f, 0.0f, 1.0f);
+}
+
 // O10 — one sparse-IR walk per thread (P:15, P:35, P:46 step 3; R9-R11)
 __global__ void k_walks(SceneView sv, BvhView bv, const uint8_t* __restrict__ labels, int64_t w0, int64_t nb,
                         int max_depth, int rr, uint64_t seed, vpl_record* __restrict__ dep, int32_t* __restrict__ cnt) {
@@ -214,10 +236,13 @@ __global__ void k_walks(SceneView sv, BvhView bv, const uint8_t* __restrict__ la
     int l = (int)(((uint64_t)x0 * (uint64_t)h->nL) >> 32);
     const float* L = h->lights + 16 * l;
     float beta[3];
-    for (int c = 0; c < 3; ++c) beta[c] = (float)(kPi * (double)L[12] * (double)L[13 + c] * (double)h->nL);
+    // beta0 = power of light l x n_L: pi A L (area light), Phi (point light, R27)
+    for (int c = 0; c < 3; ++c)
+        beta[c] = light_is_point(L) ? (float)((double)L[13 + c] * (double)h->nL)
+                                    : (float)(kPi * (double)L[12] * (double)L[13 + c] * (double)h->nL);
     float u1 = u01(rng.next()), u2 = u01(rng.next());
-    f3 o = (light_corner(L) + u1 * light_eu(L)) + u2 * light_ev(L);
-    f3 dir = malley(rng, light_n(L));
+    f3 o = (light_corner(L) + u1 * light_eu(L)) + u2 * light_ev(L);   // point light: e_u = e_v = 0
+    f3 dir = light_is_point(L) ? sphere_dir(rng) : malley(rng, light_n(L));
     const float INV_PI = (float)(1.0 / kPi);
     float eps = h->eps;
     int c_out = 0;

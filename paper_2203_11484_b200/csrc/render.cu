@@ -398,12 +398,23 @@ __global__ void k_direct(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint*
     const float4* gp = (const float4*)(gb + pix);
     const float4 a = gp[0], b = gp[1], c = gp[2];
     const bool ok = __float_as_int(a.w) >= 0 && __float_as_int(b.w) != 0;
-    float E[3] = {0.0f, 0.0f, 0.0f};
+    float E[3] = {0.0f, 0.0f, 0.0f}, Pt[3] = {0.0f, 0.0f, 0.0f};
     if (ok) {
         const f3 x = xyz(a), nx = xyz(b);
         Philox ph(seed, 4u, (uint32_t)pix);
         for (int l = 0; l < h->nL; ++l) {
             const float* L = h->lights + 16 * l;
+            if (light_is_point(L)) {   // R27: no samples, Phi cx / ((r2 sqrt r2) 4 pi) V
+                const f3 y = ld3(L);
+                const f3 d = y - x;
+                const float r2 = dot(d, d);
+                const float cx = dot(nx, d);
+                if (cx > 0.0f && !segment_occluded<false>(bv, x, y, h->eps, nullptr)) {
+                    const float gg = point_g(cx, r2);
+                    Pt[0] += L[13] * gg; Pt[1] += L[14] * gg; Pt[2] += L[15] * gg;
+                }
+                continue;
+            }
             const f3 corner = ld3(L), eu = ld3(L + 3), ev = ld3(L + 6), nl = ld3(L + 9);
             for (int q = 0; q < S; ++q) {
                 const uint32_t j = 2u * (uint32_t)(l * S + q);
@@ -422,9 +433,9 @@ __global__ void k_direct(SceneView sv, BvhView bv, TileMap tm, const vpl_gpoint*
     }
     const float INV_PI = (float)(1.0 / kPiR);
     float* o = rgb + 3 * (int64_t)pix;
-    const float r0 = ok ? (c.x * (E[0] * inv_S)) * INV_PI : 0.0f;
-    const float r1 = ok ? (c.y * (E[1] * inv_S)) * INV_PI : 0.0f;
-    const float r2o = ok ? (c.z * (E[2] * inv_S)) * INV_PI : 0.0f;
+    const float r0 = ok ? (c.x * ((E[0] * inv_S) + Pt[0])) * INV_PI : 0.0f;
+    const float r1 = ok ? (c.y * ((E[1] * inv_S) + Pt[1])) * INV_PI : 0.0f;
+    const float r2o = ok ? (c.z * ((E[2] * inv_S) + Pt[2])) * INV_PI : 0.0f;
     if (accumulate) { o[0] += r0; o[1] += r1; o[2] += r2o; }
     else { o[0] = r0; o[1] = r1; o[2] = r2o; }
 }

@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 __all__ = ["Scene", "make_scene", "CONFIGS", "custom_scene", "quad_tris", "box_tris",
-           "icosphere_tris", "room_tris", "make_light", "make_camera"]
+           "icosphere_tris", "room_tris", "make_light", "make_point_light", "point_lights_of", "make_camera"]
 
 
 @dataclass
@@ -159,6 +159,25 @@ def make_light(center, size=0.5, radiance=(10.0, 10.0, 10.0)):
     corner = c - np.array([size / 2, 0.0, size / 2])
     return np.concatenate([corner, [size, 0, 0], [0, 0, size], [0, -1, 0],
                            [size * size], list(radiance)]).astype(np.float32)
+
+
+def make_point_light(position, power=(10.0, 10.0, 10.0)):
+    """Isotropic point light (reading R27, "the light sources are all
+    point lights"): the light row with e_u = e_v = 0 and area = 0, `power`
+    (W per channel) in the radiance field."""
+    return np.concatenate([np.asarray(position, np.float64), [0, 0, 0], [0, 0, 0], [0, -1, 0], [0.0],
+                           list(power)]).astype(np.float32)
+
+
+def point_lights_of(lights, drop=0.2):
+    """The paper-literal variant of a config (R27): every area light becomes a
+    point light `drop` m below its centre with the area light's total power
+    pi * A * L (so the two variants carry the same energy)."""
+    out = []
+    for L in np.asarray(lights, np.float64):
+        c = L[0:3] + 0.5 * L[3:6] + 0.5 * L[6:9] + drop * L[9:12]
+        out.append(make_point_light(c, np.pi * L[12] * L[13:16]))
+    return np.stack(out)
 
 
 def make_camera(pos, target, vfov_deg, W, H, up=(0.0, 1.0, 0.0)):
@@ -367,10 +386,15 @@ def _finish(d):
     return Scene(verts=V, albedo=A, lights=L, cam=C, **d)
 
 
-def make_scene(config: int, seed: int | None = None, **kw) -> Scene:
-    """Build BASELINE.json configs[config-1] with its seed (BJ:7-11)."""
+def make_scene(config: int, seed: int | None = None, point_lights: bool = False, **kw) -> Scene:
+    """Build BASELINE.json configs[config-1] with its seed (BJ:7-11);
+    point_lights=True gives the paper-literal variant lit by point lights
+    (reading R27) of the same geometry and light power."""
     fn = CONFIGS[config]
     d = fn(**kw) if seed is None else fn(seed=seed, **kw)
+    if point_lights:
+        d["lights"] = point_lights_of(d["lights"])
+        d["name"] = d["name"] + "-point"
     return _finish(d)
 
 
