@@ -80,6 +80,9 @@ __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, floa
 #ifndef VPL_GATHER_CTAS
 #define VPL_GATHER_CTAS 32
 #endif
+#ifndef VPL_SMEM_NRM
+#define VPL_SMEM_NRM 0   // 1: receiver normal / triangle re-read from shared memory every VPL
+#endif
 #ifndef VPL_PART_EVICT_LAST
 #define VPL_PART_EVICT_LAST 1   // partial stores with an L2 evict_last policy (C4: DRAM writes 120 -> 64 MB per launch)
 #endif
@@ -101,6 +104,9 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                                                 int* __restrict__ slot_gen, int32_t ring, GatherDump dump) {
     __shared__ int sstack[kWarpStack];
     __shared__ float s_acc[3][32];   // running per-lane totals (kept out of the register budget)
+#if VPL_SMEM_NRM
+    __shared__ float4 s_nt[32];      // receiver normal + (active ? tri_x : -1), re-read per VPL (no spill)
+#endif
     const int lane = threadIdx.x;
     const int64_t ntask = tm.n_warps() * n_chunks;
     const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
@@ -126,6 +132,10 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             active = tri_x >= 0 && __float_as_int(b.w) != 0;
             x = xyz(a); nx = xyz(b);
         }
+#if VPL_SMEM_NRM
+        s_nt[lane] = make_float4(nx.x, nx.y, nx.z, __int_as_float(active ? tri_x : -1));
+        __syncwarp();
+#endif
         s_acc[0][lane] = 0.0f; s_acc[1][lane] = 0.0f; s_acc[2][lane] = 0.0f;
         OccluderCache cache;
         TravStats st;
@@ -149,8 +159,18 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                         int yt[kGroup];
                         const int gsz = group_at(vpls, i, c1, xr, yk, yt);
                         float w[kGroup];
+#if VPL_SMEM_NRM
+                        float4 ntv;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(ntv.x), "=f"(ntv.y), "=f"(ntv.z), "=f"(ntv.w)
+                                     : "r"((unsigned)__cvta_generic_to_shared(s_nt + lane)));
+                        const int tri_l = __float_as_int(ntv.w);
+                        const unsigned tv = shade_group<kCount>(bv, vpls, i, gsz, yk, yt, x, xyz(ntv), tri_l, tri_l >= 0,
+                                                                eps, b2, cache, sstack, &st, w, cand, cand_end, c1, inc);
+#else
                         const unsigned tv = shade_group<kCount>(bv, vpls, i, gsz, yk, yt, x, nx, tri_x, active, eps, b2,
                                                                 cache, sstack, &st, w, cand, cand_end, c1, inc);
+#endif
                         const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
                         if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
                         if (kDump && dslot >= 0) {
