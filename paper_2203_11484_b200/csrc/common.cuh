@@ -596,30 +596,22 @@ __device__ __forceinline__ vpl_gpoint primary_hit(const SceneView& sv, const Bvh
     return o;
 }
 
-// tile -> pixel mapping: warp w of a call covers an 8x4 block
+// tile -> pixel mapping: warp w of a call covers an 8 x bh block (bh = 4, or 8 for the gather with two
+// receivers per lane: lane l holds (l % 8, l / 8 + 4k), k = 0, 1)
 struct TileMap {
     const int32_t* tiles;
     int32_t n_tiles, tw, th, W, H, tiles_x, blocks_per_tile, bx_per_tile;
+    int32_t bh = 4;
     __host__ __device__ int64_t n_warps() const { return (int64_t)n_tiles * blocks_per_tile; }
-    // index of the 8x4 block of warp g in the frame's block grid (ceil(W/8) per row), or -1 when the
-    // block lies wholly outside the image (tiles may overhang the last row / column)
-    __device__ __forceinline__ int64_t block_index(int64_t g) const {
-        int32_t ti = (int32_t)(g / blocks_per_tile), sub = (int32_t)(g % blocks_per_tile);
-        int32_t t = tiles[ti];
-        int32_t tx = t % tiles_x, ty = t / tiles_x;
-        int32_t x0 = tx * tw + (sub % bx_per_tile) * 8;
-        int32_t y0 = ty * th + (sub / bx_per_tile) * 4;
-        if (x0 >= W || y0 >= H) return -1;
-        return (int64_t)(y0 / 4) * ((W + 7) / 8) + x0 / 8;
-    }
-    // returns the pixel of (warp g, lane) or -1 when outside the image
-    __device__ __forceinline__ int32_t pixel(int64_t g, int lane) const {
+    // returns the pixel of (warp g, lane, receiver k) or -1 when outside the image
+    __device__ __forceinline__ int32_t pixel(int64_t g, int lane, int k = 0) const {
         int32_t ti = (int32_t)(g / blocks_per_tile), sub = (int32_t)(g % blocks_per_tile);
         int32_t t = tiles[ti];
         int32_t tx = t % tiles_x, ty = t / tiles_x;
         int32_t x = tx * tw + (sub % bx_per_tile) * 8 + (lane & 7);
-        int32_t y = ty * th + (sub / bx_per_tile) * 4 + (lane >> 3);
-        return (x < W && y < H) ? y * W + x : -1;
+        int32_t yt = (sub / bx_per_tile) * bh + (lane >> 3) + 4 * k;   // row inside the tile
+        int32_t y = ty * th + yt;
+        return (x < W && y < H && yt < th) ? y * W + x : -1;
     }
 };
 

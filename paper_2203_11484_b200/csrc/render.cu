@@ -80,9 +80,6 @@ __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, floa
 #ifndef VPL_GATHER_CTAS
 #define VPL_GATHER_CTAS 32
 #endif
-#ifndef VPL_SMEM_NRM
-#define VPL_SMEM_NRM 0   // 1: receiver normal / triangle re-read from shared memory every VPL
-#endif
 #ifndef VPL_PART_EVICT_LAST
 #define VPL_PART_EVICT_LAST 1   // partial stores with an L2 evict_last policy (C4: DRAM writes 120 -> 64 MB per launch)
 #endif
@@ -103,10 +100,8 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                                                 float* __restrict__ part_out, int* __restrict__ done,
                                                 int* __restrict__ slot_gen, int32_t ring, GatherDump dump) {
     __shared__ int sstack[kWarpStack];
-    __shared__ float s_acc[3][32];   // running per-lane totals (kept out of the register budget)
-#if VPL_SMEM_NRM
-    __shared__ float4 s_nt[32];      // receiver normal + (active ? tri_x : -1), re-read per VPL (no spill)
-#endif
+    __shared__ float s_acc[kSeg][3][32];   // running per-receiver totals (kept out of the register budget)
+    constexpr int kPart = 96 * kSeg;       // partial floats per (block, chunk): 32 lanes x kSeg receivers x 3
     const int lane = threadIdx.x;
     const int64_t ntask = tm.n_warps() * n_chunks;
     const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
@@ -115,106 +110,104 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
         if (lane == 0) g = atomicAdd(queue, 1);
         g = __shfl_sync(0xFFFFFFFFu, g, 0);
         if (g >= ntask) break;
-        // task = (8x4 pixel block, VPL chunk): fine-grained enough that the dynamic queue balances
+        // task = (8 x 4kSeg pixel block, VPL chunk): fine-grained enough that the dynamic queue balances
         // the SMs even when a rank holds 1/8 of the frame
         const int ch = (int)(g % n_chunks);
         const int vbeg = ch * chunk, vend = min(M, vbeg + chunk);
-        int32_t pix = tm.pixel(g / n_chunks, lane);
-        bool active = false;
-        f3 x = mk3(0, 0, 0), nx = mk3(0, 0, 0);
-        int tri_x = -1;
-        int dslot = -1;
-        if (kDump && pix >= 0) dslot = dump.slot[pix];
-        if (pix >= 0) {
-            const float4* gp = (const float4*)(gb + pix);
-            float4 a = gp[0], b = gp[1];
-            tri_x = __float_as_int(a.w);
-            active = tri_x >= 0 && __float_as_int(b.w) != 0;
-            x = xyz(a); nx = xyz(b);
+        int32_t pix[kSeg];
+        f3 x[kSeg], nx[kSeg];
+        int tri_x[kSeg];
+        unsigned act = 0;
+#pragma unroll
+        for (int k = 0; k < kSeg; ++k) {
+            pix[k] = tm.pixel(g / n_chunks, lane, k);
+            x[k] = mk3(0, 0, 0); nx[k] = mk3(0, 0, 0);
+            tri_x[k] = -1;
+            if (pix[k] >= 0) {
+                const float4* gp = (const float4*)(gb + pix[k]);
+                const float4 a = gp[0], b = gp[1];
+                tri_x[k] = __float_as_int(a.w);
+                if (tri_x[k] >= 0 && __float_as_int(b.w) != 0) act |= 1u << k;
+                x[k] = xyz(a); nx[k] = xyz(b);
+            }
+            s_acc[k][0][lane] = 0.0f; s_acc[k][1][lane] = 0.0f; s_acc[k][2][lane] = 0.0f;
         }
-#if VPL_SMEM_NRM
-        s_nt[lane] = make_float4(nx.x, nx.y, nx.z, __int_as_float(active ? tri_x : -1));
-        __syncwarp();
-#endif
-        s_acc[0][lane] = 0.0f; s_acc[1][lane] = 0.0f; s_acc[2][lane] = 0.0f;
-        OccluderCache cache;
+        OccluderCache cache[kSeg];
         TravStats st;
         unsigned long long n_traced = 0, n_vis = 0;
-        const unsigned am = __ballot_sync(0xFFFFFFFFu, active);
-        if (am) {
-            const int l0 = __ffs(am) - 1;
-            const f3 xr = mk3(__shfl_sync(0xFFFFFFFFu, x.x, l0), __shfl_sync(0xFFFFFFFFu, x.y, l0),
-                              __shfl_sync(0xFFFFFFFFu, x.z, l0));
+        if (__any_sync(0xFFFFFFFFu, act != 0)) {
             for (int i0 = vbeg; i0 < vend; i0 += 256) {
-                float part[3] = {0.0f, 0.0f, 0.0f};
+                float part[kSeg][3];
+#pragma unroll
+                for (int k = 0; k < kSeg; ++k) part[k][0] = part[k][1] = part[k][2] = 0.0f;
                 const int i1 = min(vend, i0 + 256);
                 for (int c0 = i0; c0 < i1; c0 += kCluster) {       // clusters of kCluster VPLs (i0 % 256 == 0)
                     const float4* cb = clusters ? clusters + 4 * (c0 / kCluster) : nullptr;
-                    const bool inc = active && (!cb || cluster_may_trace(cb, x, nx));   // lane may trace it
-                    if (cb && !__any_sync(0xFFFFFFFFu, inc)) continue;   // no lane can trace any VPL of it
+                    unsigned inc = act;                            // receivers that may trace the cluster
+#pragma unroll
+                    for (int k = 0; k < kSeg; ++k)
+                        if (cb && ((inc >> k) & 1u) && !cluster_may_trace(cb, x[k], nx[k])) inc &= ~(1u << k);
+                    if (cb && !__any_sync(0xFFFFFFFFu, inc != 0)) continue;   // no receiver can trace any VPL of it
                     const int c1 = min(c0 + kCluster, i1);
                     int cand = -1, cand_end = cb ? c0 : INT_MAX;           // candidate list (lazy) and its VPL range end
-                    for (int i = c0; i < c1;) {
-                        f3 yk[kGroup];
-                        int yt[kGroup];
-                        const int gsz = group_at(vpls, i, c1, xr, yk, yt);
-                        float w[kGroup];
-#if VPL_SMEM_NRM
-                        float4 ntv;
-                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(ntv.x), "=f"(ntv.y), "=f"(ntv.z), "=f"(ntv.w)
-                                     : "r"((unsigned)__cvta_generic_to_shared(s_nt + lane)));
-                        const int tri_l = __float_as_int(ntv.w);
-                        const unsigned tv = shade_group<kCount>(bv, vpls, i, gsz, yk, yt, x, xyz(ntv), tri_l, tri_l >= 0,
-                                                                eps, b2, cache, sstack, &st, w, cand, cand_end, c1, inc);
-#else
-                        const unsigned tv = shade_group<kCount>(bv, vpls, i, gsz, yk, yt, x, nx, tri_x, active, eps, b2,
-                                                                cache, sstack, &st, w, cand, cand_end, c1, inc);
-#endif
+                    for (int i = c0; i < c1; ++i) {
+                        const float4 yv = __ldg((const float4*)(vpls + i));
+                        float w[kSeg];
+                        const unsigned tv = shade<kCount>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), x, nx, tri_x, act,
+                                                          eps, b2, cache, sstack, &st, w, cand, cand_end, c1, inc);
                         const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
                         if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
-                        if (kDump && dslot >= 0) {
-                            for (int k = 0; k < gsz; ++k) {
-                                const int o = dump.perm ? dump.perm[i + k] : i + k;
-                                const size_t wd = (size_t)dslot * dump.words + (o >> 5);
-                                if (tr & (1u << k)) atomicOr(dump.tbits + wd, 1u << (o & 31));
-                                if (vis & (1u << k)) atomicOr(dump.vbits + wd, 1u << (o & 31));
-                            }
-                        }
+                        if (kDump) {
 #pragma unroll
-                        for (int k = 0; k < kGroup; ++k) {
-                            if (vis & (1u << k)) {
-                                const float4 phi = __ldg((const float4*)(vpls + i + k) + 2);
-                                part[0] = fmaf(phi.x, w[k], part[0]);
-                                part[1] = fmaf(phi.y, w[k], part[1]);
-                                part[2] = fmaf(phi.z, w[k], part[2]);
+                            for (int k = 0; k < kSeg; ++k) {
+                                const int ds = pix[k] >= 0 ? dump.slot[pix[k]] : -1;
+                                if (ds >= 0) {
+                                    const int o = dump.perm ? dump.perm[i] : i;
+                                    const size_t wd = (size_t)ds * dump.words + (o >> 5);
+                                    if (tr & (1u << k)) atomicOr(dump.tbits + wd, 1u << (o & 31));
+                                    if (vis & (1u << k)) atomicOr(dump.vbits + wd, 1u << (o & 31));
+                                }
                             }
                         }
-                        i += gsz;
+                        if (vis) {
+                            const float4 phi = __ldg((const float4*)(vpls + i) + 2);
+#pragma unroll
+                            for (int k = 0; k < kSeg; ++k)
+                                if (vis & (1u << k)) {
+                                    part[k][0] = fmaf(phi.x, w[k], part[k][0]);
+                                    part[k][1] = fmaf(phi.y, w[k], part[k][1]);
+                                    part[k][2] = fmaf(phi.z, w[k], part[k][2]);
+                                }
+                        }
                     }
                 }
-                s_acc[0][lane] += part[0]; s_acc[1][lane] += part[1]; s_acc[2][lane] += part[2];
+#pragma unroll
+                for (int k = 0; k < kSeg; ++k) {
+                    s_acc[k][0][lane] += part[k][0]; s_acc[k][1][lane] += part[k][1]; s_acc[k][2][lane] += part[k][2];
+                }
             }
         }
-        if (pix >= 0) {
-            if (n_chunks == 1) {
-                const float s = (float)(1.0 / kPiR);
-                f3 rho = xyz(((const float4*)(gb + pix))[2]);
-                float* o = rgb + 3 * (int64_t)pix;
-                o[0] = active ? s_acc[0][lane] * rho.x * s : 0.0f;
-                o[1] = active ? s_acc[1][lane] * rho.y * s : 0.0f;
-                o[2] = active ? s_acc[2][lane] * rho.z * s : 0.0f;
-            }
+        const float sc = (float)(1.0 / kPiR);
+        if (n_chunks == 1) {
+#pragma unroll
+            for (int k = 0; k < kSeg; ++k)
+                if (pix[k] >= 0) {
+                    const bool on = (act >> k) & 1u;
+                    const f3 rho = xyz(((const float4*)(gb + pix[k]))[2]);
+                    float* o = rgb + 3 * (int64_t)pix[k];
+                    o[0] = on ? s_acc[k][0][lane] * rho.x * sc : 0.0f;
+                    o[1] = on ? s_acc[k][1][lane] * rho.y * sc : 0.0f;
+                    o[2] = on ? s_acc[k][2][lane] * rho.z * sc : 0.0f;
+                }
         }
-        VPL_DCHECK(pix < (int64_t)tm.W * tm.H);
         if (n_chunks > 1) {
-            // chunk partial sums, (slot, chunk, lane)-contiguous in a ring of `ring` block slots (the
-            // call's block ordinal modulo ring: a few MB stay L2-resident); the warp that completes a
-            // block's last chunk folds them in chunk order (fp32), writes the pixels, discards the
-            // partial lines (never written back to HBM) and hands the slot to the block `ring` later.
+            // chunk partial sums, (slot, chunk, receiver, lane)-contiguous in a ring of `ring` block slots
+            // (the call's block ordinal modulo ring: a few MB stay L2-resident); the warp that completes a
+            // block's last chunk folds them in chunk order (fp32), writes the pixels, discards the partial
+            // lines (never written back to HBM) and hands the slot to the block `ring` later.
             const int64_t lb = g / n_chunks;
             const int slot = (int)(lb % ring), gen = (int)(lb / ring);
-            float* pb = part_out + ((int64_t)slot * n_chunks) * 96;   // 96 floats = 32 lanes x 3 = 3 lines
+            float* pb = part_out + ((int64_t)slot * n_chunks) * kPart;
             if (lane == 0) {   // the slot's previous block (dispensed earlier, so running) must be folded
                 int cur;
                 while (true) {
@@ -224,18 +217,19 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 }
             }
             __syncwarp();
-            float* o = pb + ch * 96 + 3 * lane;
+#pragma unroll
+            for (int k = 0; k < kSeg; ++k) {
+                float* o = pb + ch * kPart + 96 * k + 3 * lane;
 #if VPL_PART_EVICT_LAST
-            {   // keep the partial lines in L2 until the fold discards them
-                uint64_t pol;
+                uint64_t pol;   // keep the partial lines in L2 until the fold discards them
                 asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-                asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(o), "f"(s_acc[0][lane]), "l"(pol) : "memory");
-                asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(o + 1), "f"(s_acc[1][lane]), "l"(pol) : "memory");
-                asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(o + 2), "f"(s_acc[2][lane]), "l"(pol) : "memory");
-            }
+                asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(o), "f"(s_acc[k][0][lane]), "l"(pol) : "memory");
+                asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(o + 1), "f"(s_acc[k][1][lane]), "l"(pol) : "memory");
+                asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(o + 2), "f"(s_acc[k][2][lane]), "l"(pol) : "memory");
 #else
-            o[0] = s_acc[0][lane]; o[1] = s_acc[1][lane]; o[2] = s_acc[2][lane];
+                o[0] = s_acc[k][0][lane]; o[1] = s_acc[k][1][lane]; o[2] = s_acc[k][2][lane];
 #endif
+            }
             __threadfence();
             __syncwarp();
             int prev = 0;
@@ -243,21 +237,24 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             prev = __shfl_sync(0xFFFFFFFFu, prev, 0);
             if (prev == n_chunks - 1) {
                 __threadfence();
-                float acc[3] = {0.0f, 0.0f, 0.0f};
-                for (int c = 0; c < n_chunks; ++c) {
-                    const float* q = pb + c * 96 + 3 * lane;
-                    acc[0] += __ldcg(q); acc[1] += __ldcg(q + 1); acc[2] += __ldcg(q + 2);
-                }
-                if (pix >= 0) {
-                    const float s = (float)(1.0 / kPiR);
-                    f3 rho = xyz(((const float4*)(gb + pix))[2]);
-                    float* out = rgb + 3 * (int64_t)pix;
-                    out[0] = active ? acc[0] * rho.x * s : 0.0f;
-                    out[1] = active ? acc[1] * rho.y * s : 0.0f;
-                    out[2] = active ? acc[2] * rho.z * s : 0.0f;
+#pragma unroll
+                for (int k = 0; k < kSeg; ++k) {
+                    float acc[3] = {0.0f, 0.0f, 0.0f};
+                    for (int c = 0; c < n_chunks; ++c) {
+                        const float* q = pb + c * kPart + 96 * k + 3 * lane;
+                        acc[0] += __ldcg(q); acc[1] += __ldcg(q + 1); acc[2] += __ldcg(q + 2);
+                    }
+                    if (pix[k] >= 0) {
+                        const bool on = (act >> k) & 1u;
+                        const f3 rho = xyz(((const float4*)(gb + pix[k]))[2]);
+                        float* out = rgb + 3 * (int64_t)pix[k];
+                        out[0] = on ? acc[0] * rho.x * sc : 0.0f;
+                        out[1] = on ? acc[1] * rho.y * sc : 0.0f;
+                        out[2] = on ? acc[2] * rho.z * sc : 0.0f;
+                    }
                 }
                 __syncwarp();
-                for (int l = lane; l < 3 * n_chunks; l += 32)
+                for (int l = lane; l < (kPart / 32) * n_chunks; l += 32)
                     asm volatile("discard.global.L2 [%0], 128;" ::"l"(pb + 32 * l) : "memory");
                 __syncwarp();
                 if (lane == 0) {
@@ -268,7 +265,7 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             }
         }
         if (kCount) {
-            unsigned long long pairs = active ? (unsigned long long)(vend - vbeg) : 0ull;
+            unsigned long long pairs = (unsigned long long)__popc(act) * (unsigned long long)(vend - vbeg);
             unsigned long long v[19] = {pairs, n_traced, n_vis, st.boxes, st.tris, st.wrays, st.wsteps,
                                         st.cones, st.cpk, st.rpk, st.chits, st.ctests, st.lists, st.entries,
                                         st.lfail, st.fsteps, st.lsteps, st.fmt, st.fmt_hit};
@@ -283,42 +280,37 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
 }
 
 // test hook: traced / visible bits of listed pixels x all VPLs, through the
-// gather's own group / beam traversal (lanes = 32 consecutive listed pixels)
+// gather's own traversal engine in the caller's VPL order (lanes = 32
+// consecutive listed pixels, receiver slot 0; no clusters, no lists)
 __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict__ gb, const vpl_record* __restrict__ vpls,
                           int32_t M, const int32_t* __restrict__ pixels, int32_t n_px, uint32_t* __restrict__ tbits,
                           uint32_t* __restrict__ vbits) {
     __shared__ int s_stack[2][kWarpStack];
     int* sstack = s_stack[threadIdx.x >> 5];
     int64_t words = (M + 31) / 32;
-    OccluderCache cache;
+    OccluderCache cache[kSeg];
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     if ((k - lane) >= n_px) return;                      // whole warp out of range
     bool inb = k < n_px;
     const vpl_gpoint* gp = gb + (inb ? pixels[k] : 0);
-    bool active = inb && gp->tri >= 0 && gp->front;
-    f3 x = ld3(gp->pos), nx = ld3(gp->nrm);
-    int tri_x = gp->tri;
+    f3 x[kSeg], nx[kSeg];
+    int tri_x[kSeg];
+    x[0] = ld3(gp->pos); nx[0] = ld3(gp->nrm); tri_x[0] = gp->tri;
+    if (kSeg > 1) { x[kSeg - 1] = x[0]; nx[kSeg - 1] = nx[0]; tri_x[kSeg - 1] = -1; }
+    const unsigned act = (inb && gp->tri >= 0 && gp->front) ? 1u : 0u;
     const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
-    const unsigned am = __ballot_sync(0xFFFFFFFFu, active);
-    const int l0 = am ? __ffs(am) - 1 : 0;
-    const f3 xr = mk3(__shfl_sync(0xFFFFFFFFu, x.x, l0), __shfl_sync(0xFFFFFFFFu, x.y, l0),
-                      __shfl_sync(0xFFFFFFFFu, x.z, l0));
     for (int64_t wd = 0; wd < words; ++wd) {
         uint32_t tb = 0, vb = 0;
         const int i0 = (int)(wd * 32), i1 = min(M, i0 + 32);
-        for (int i = i0; i < i1;) {
-            f3 yk[kGroup];
-            int yt[kGroup];
-            const int gsz = group_at(vpls, i, i1, xr, yk, yt);
-            float w[kGroup];
-            int cand = -1, cand_end = INT_MAX;   // the visibility dump walks the caller's order: tree traversal only
-            const unsigned tv = shade_group<false>(bv, vpls, i, gsz, yk, yt, x, nx, tri_x, active, eps, b2, cache, sstack,
-                                                   nullptr, w, cand, cand_end, i1, active);
-            const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
-            tb |= tr << (i - i0);
-            vb |= vis << (i - i0);
-            i += gsz;
+        for (int i = i0; i < i1; ++i) {
+            const float4 yv = __ldg((const float4*)(vpls + i));
+            float w[kSeg];
+            int cand = -1, cand_end = INT_MAX;
+            const unsigned tv = shade<false>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), x, nx, tri_x, act, eps, b2,
+                                             cache, sstack, nullptr, w, cand, cand_end, i1, act);
+            tb |= (tv & 1u) << (i - i0);
+            vb |= ((tv >> 16) & 1u) << (i - i0);
         }
         if (inb) { tbits[k * words + wd] = tb; vbits[k * words + wd] = vb; }
     }
@@ -534,7 +526,7 @@ static size_t gather_layout(int32_t M, int32_t W, int32_t H, char* base, GatherW
     gather_chunks(M, &chunk, &nch);
     const size_t nblk = (size_t)((W + 7) / 8) * (size_t)((H + 3) / 4);   // 8x4 blocks of a full frame
     w->ring = (int32_t)(nblk < (size_t)VPL_PART_RING ? (nblk > 0 ? nblk : 1) : VPL_PART_RING);
-    w->part = b.take<float>(nch > 1 ? (size_t)w->ring * (size_t)nch * 96 : 1);
+    w->part = b.take<float>(nch > 1 ? (size_t)w->ring * (size_t)nch * 96 * kSeg : 1);
     w->done = b.take<int>(w->ring);
     w->slot_gen = b.take<int>(w->ring);
     w->box = b.take<unsigned>(6);
@@ -618,6 +610,8 @@ static int32_t gather_impl(const void* d_scene, const void* d_bvh, const vpl_gpo
     gather_chunks(n_vpls, &chunk, &n_chunks);
     TileMap tm;
     VPL_TRY(make_tilemap(hh, d_tiles, n_tiles, tile_w, tile_h, &tm));
+    tm.bh = 4 * kSeg;   // warps cover 8 x 4kSeg blocks (rows past a tile's end are masked)
+    tm.blocks_per_tile = (tile_w / 8) * ((tile_h + tm.bh - 1) / tm.bh);
     if (n_tiles == 0) return VPL_OK;
     int* queue = w.queue;
     VPL_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
