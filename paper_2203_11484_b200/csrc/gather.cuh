@@ -115,13 +115,14 @@ struct Segs {
 
 // exact MT (O9) of the segments in `mask` against one triangle (the any-hit form of readings
 // R25/R26: division-free, fused products in a fixed order — identical operations to mt_any)
-template <bool kCount>
+// (k0, k1): the segment slots evaluated (all of them, or the one slot of a receiver's own cache test)
+template <bool kCount, int k0 = 0, int k1 = kSeg>
 __device__ __forceinline__ unsigned mt_segs(const Segs& S, unsigned mask, float tmin, float4 a, float4 b, float4 c,
                                             TravStats* st) {
     const f3 v0 = xyz(a), e1 = xyz(b), e2 = xyz(c);
     unsigned hit = 0;
 #pragma unroll
-    for (int k = 0; k < kSeg; ++k) {
+    for (int k = k0; k < k1; ++k) {
         if (kCount && (mask & (1u << k))) st->tris += 1;
         const f3 s = S.o[k] - v0;
         const f3 q = cross_fma(s, e1);
@@ -151,12 +152,12 @@ __device__ __forceinline__ void cache_found(OccluderCache* cache, unsigned h, in
         if (h & (1u << k)) cache[k].found(tri);
 }
 
-template <bool kCount>
+template <bool kCount, int k0 = 0, int k1 = kSeg>
 __device__ __forceinline__ void test_tri(const BvhView& bv, Segs& S, unsigned mask, float tmin, int tri,
                                          OccluderCache* cache, TravStats* st) {
     if (mask) {
         const float4* tr = bv.tris + 3 * tri;
-        const unsigned h = mt_segs<kCount>(S, mask, tmin, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), st);
+        const unsigned h = mt_segs<kCount, k0, k1>(S, mask, tmin, __ldg(tr), __ldg(tr + 1), __ldg(tr + 2), st);
         if (h) {
             S.occ |= h;
             S.pend &= ~h;
@@ -511,6 +512,21 @@ __device__ __forceinline__ void resolve(const BvhView& bv, Segs& S, float eps, f
     S.pend = 0;
 }
 
+// receiver k's segment against its own recent occluders (only slot k's MT is evaluated)
+template <bool kCount, int k>
+__device__ __forceinline__ void cache_tests(const BvhView& bv, Segs& S, float eps, OccluderCache* cache,
+                                            TravStats* st) {
+    const unsigned bit = 1u << k;
+#if VPL_CACHE_STREAK
+    const unsigned m = cache[k].vis_streak ? 0u : (S.pend & bit);
+#else
+    const unsigned m = S.pend & bit;
+#endif
+    if (m && cache[k].own0 >= 0) test_tri<kCount, k, k + 1>(bv, S, m, eps, cache[k].own0, cache, st);
+    if (VPL_CACHE_OWN2 && (S.pend & m) && cache[k].own1 >= 0)
+        test_tri<kCount, k, k + 1>(bv, S, S.pend & m, eps, cache[k].own1, cache, st);
+}
+
 // One VPL (position y, triangle yt; uniform) for one lane's receivers: Eq. 1 terms (O13, exact fp32
 // order), segment setup (O9), occluder caches, resolution.  act: bit k = receiver k is a front-face
 // hit.  Returns traced | vis << 16 (bit k per receiver) and w[k] = cx*ci / (r2 * max(r2, b2)).
@@ -556,18 +572,10 @@ __device__ __forceinline__ unsigned shade(const BvhView& bv, const vpl_record* _
     // whose last traced segment was visible skips its cache (visibility is coherent along the
     // spatially ordered VPLs)
     const uint32_t t0 = kCount ? st->tris : 0;
-#pragma unroll
-    for (int k = 0; k < kSeg; ++k) {
-        const unsigned bit = 1u << k;
-#if VPL_CACHE_STREAK
-        const unsigned m = cache[k].vis_streak ? 0u : (S.pend & bit);
-#else
-        const unsigned m = S.pend & bit;
-#endif
-        if (m && cache[k].own0 >= 0) test_tri<kCount>(bv, S, m, eps, cache[k].own0, cache, st);
-        if (VPL_CACHE_OWN2 && (S.pend & m) && cache[k].own1 >= 0)
-            test_tri<kCount>(bv, S, S.pend & m, eps, cache[k].own1, cache, st);
-    }
+    cache_tests<kCount, 0>(bv, S, eps, cache, st);
+    if (kSeg > 1) cache_tests<kCount, (kSeg > 1 ? 1 : 0)>(bv, S, eps, cache, st);
+    if (kSeg > 2) cache_tests<kCount, (kSeg > 2 ? 2 : 0)>(bv, S, eps, cache, st);
+    if (kSeg > 3) cache_tests<kCount, (kSeg > 3 ? 3 : 0)>(bv, S, eps, cache, st);
     if (kCount) { st->chits += __popc(S.occ); st->ctests += st->tris - t0; }
     resolve<kCount>(bv, S, eps, y, cache, sstack, st, cand, cand_end, cend, part, xr, vpls, i);
     const unsigned vis = traced & ~S.occ;
