@@ -199,6 +199,25 @@ __device__ __forceinline__ bool make_beam(const Segs& S, f3 y, float eps, Beam& 
 
 // Beam {y + s*D : y in [yl, yh], D in [Dn, Dm], s in [s_lo, s_hi]} from uniform bounds; lmin / lmax
 // bound the segment lengths from below / above.  Returns false if the beam is loose.
+//
+// A "straddling" axis (D changes sign on it: the VPL and the receivers overlap along it) has no
+// s-interval; it is encoded in the same two-FFMA slab form as an extent test of the segment points'
+// range [L, U] = [yl + Dn, yh + Dm] on that axis (s in [0, 1]):  with N = lo, F = hi and a power of
+// two G = 2^21 / 2^e (2^e >= max(|L|, |U|, 1), so L*G and U*G are exact and |.| < 2^21),
+//   s0 = lo*G - (U*G + 2)  <= -2 + rounding < 0   whenever lo <= U,
+//   s1 = hi*G - (L*G - 2)  >=  2 - rounding > 1   whenever hi >= L,
+// i.e. neutral for every box that meets [L, U] (conservative), and s0 > s_hi (or s1 < s_lo) once the
+// box misses it by more than 3 / G.
+#ifndef VPL_STRADDLE_BEAM
+#define VPL_STRADDLE_BEAM 1   // per-VPL beams with straddling axes instead of per-ray packets
+#endif
+__device__ __forceinline__ void straddle_axis(float L, float U, float& a0, float& b0, float& a1, float& b1) {
+    const float m = fmaxf(fmaxf(fabsf(L), fabsf(U)), 1.0f);
+    const int e = ((__float_as_int(m) >> 23) & 0xFF) - 126;          // m < 2^e
+    const float G = __int_as_float((127 + 21 - e) << 23);              // 2^(21 - e)
+    a0 = G; b0 = U * G + 2.0f;
+    a1 = G; b1 = L * G - 2.0f;
+}
 __device__ __forceinline__ bool beam_from_bounds(const float* Dn, const float* Dm, const float* yl, const float* yh,
                                                  float lmin, float lmax, float spread_tol, float eps, Beam& B) {
     const float spread = fmax3(Dm[0] - Dn[0], Dm[1] - Dn[1], Dm[2] - Dn[2]);
@@ -207,8 +226,8 @@ __device__ __forceinline__ bool beam_from_bounds(const float* Dn, const float* D
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         const bool p = Dn[a] > 0.0f, n = Dm[a] < 0.0f;
-        tight &= p | n;
-        if (p) B.pos |= 1u << a;
+        if (!VPL_STRADDLE_BEAM) tight &= p | n;
+        if (p || !n) B.pos |= 1u << a;   // straddling: N = lo, F = hi
         // approximate reciprocals: a0 and b0 = y*a0 share the same a0, so s is scaled by
         // (1 + 2^-22) at most — a position error far below the box padding
         const float rmax = rcp_approx(Dm[a]), rmin = rcp_approx(Dn[a]);
@@ -216,6 +235,8 @@ __device__ __forceinline__ bool beam_from_bounds(const float* Dn, const float* D
         B.b0[a] = (p ? yh[a] : yl[a]) * B.a0[a];
         B.a1[a] = p ? rmin : rmax;
         B.b1[a] = (p ? yl[a] : yh[a]) * B.a1[a];
+        if (VPL_STRADDLE_BEAM && !p && !n)
+            straddle_axis(yl[a] + Dn[a], yh[a] + Dm[a], B.a0[a], B.b0[a], B.a1[a], B.b1[a]);
     }
     // segment (x_j, y_k) tests t in (eps, L - eps): s = 1 - t/L in (eps/L, 1 - eps/L) within
     // [eps/Lmax, 1 - eps/Lmax]; half the cap is cut (the rest is slack for MT's rounding of t)
@@ -255,10 +276,10 @@ __device__ __forceinline__ bool make_cluster_beam(const float* xl, const float* 
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         const bool sa = !(Dn[a] > 0.0f) && !(Dm[a] < 0.0f);
-        C.L[a] = sa ? yl[a] + Dn[a] : -inf;
-        C.U[a] = sa ? yh[a] + Dm[a] : inf;
-        if (sa) {
-            ++straddle;
+        C.L[a] = sa && !VPL_STRADDLE_BEAM ? yl[a] + Dn[a] : -inf;
+        C.U[a] = sa && !VPL_STRADDLE_BEAM ? yh[a] + Dm[a] : inf;
+        if (sa) ++straddle;
+        if (sa && !VPL_STRADDLE_BEAM) {   // (VPL_STRADDLE_BEAM: beam_from_bounds encoded the extent test)
             C.B.pos |= 1u << a;   // N = lo, F = hi
             C.B.a0[a] = 0.0f; C.B.b0[a] = inf;
             C.B.a1[a] = 0.0f; C.B.b1[a] = -inf;
@@ -267,6 +288,7 @@ __device__ __forceinline__ bool make_cluster_beam(const float* xl, const float* 
     return VPL_CAND_STRADDLE ? straddle < 3 : straddle == 0;
 }
 __device__ __forceinline__ bool cluster_beam_box(const ClusterBeam& C, float4 lo, float4 hi) {
+    if (VPL_STRADDLE_BEAM) return beam_box(C.B, lo, hi);
     const bool ext = (lo.x <= C.U[0]) & (lo.y <= C.U[1]) & (lo.z <= C.U[2]) & (hi.x >= C.L[0]) &
                      (hi.y >= C.L[1]) & (hi.z >= C.L[2]);
     return ext & beam_box(C.B, lo, hi);
