@@ -93,4 +93,4 @@ def main(csv_path, sass_path, kern, srcdir="paper_2203_11484_b200/csrc"):
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])
