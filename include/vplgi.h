@@ -42,7 +42,7 @@ extern "C" {
 #define VPL_API
 #endif
 
-#define VPL_ABI_VERSION 3   /* 3: vpl_counters.cand_*, filter_steps; 2: vpl_gather_bytes(M, W, H), vpl_counters.cache_tests, f1-f4 entry points */
+#define VPL_ABI_VERSION 4   /* 4: vpl_counters.plane_culled; 3: vpl_counters.cand_*, filter_steps; 2: vpl_gather_bytes(M, W, H), vpl_counters.cache_tests, f1-f4 entry points */
 #define VPL_MAX_LIGHTS 64
 
 enum {
@@ -141,6 +141,7 @@ typedef struct {
     unsigned long long cand_steps;   /* traversal steps spent building the lists (part of warp_steps) */
     unsigned long long filter_mt;    /* warp-level MT tests issued by the list filter */
     unsigned long long filter_mt_hits; /* ... of which found an occluder for some lane */
+    unsigned long long plane_culled; /* box-hit candidate triangles dropped by the plane-side cull before MT */
 } vpl_counters;
 
 /* -------------------------------------------------------------------- */
@@ -241,9 +242,10 @@ VPL_API int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, cons
  * the dump row of each pixel or -1; d_traced_bits / d_vis_bits:
  * uint32[rows * ceil(n_vpls/32)], zeroed by the caller, bit i%32 of word i/32
  * = VPL i of d_vpls (the caller's order).  d_ctr nullable.  flags:
- * VPL_GATHER_NO_CULL runs without the VPL-cluster cull and the candidate
- * lists (plain per-VPL beam traversal), so the counters of the two runs can
- * be compared. */
+ * VPL_GATHER_NO_CULL runs without the VPL-cluster cull, the candidate
+ * lists and the plane-side cull (plain per-VPL beam traversal, an exact MT
+ * for every triangle box the beam reaches), so the counters of the two runs
+ * can be compared. */
 enum { VPL_GATHER_NO_CULL = 1 };
 VPL_API int32_t vpl_gather_dump(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf,
                                 const vpl_record* d_vpls, int32_t n_vpls, const int32_t* d_tiles, int32_t n_tiles,

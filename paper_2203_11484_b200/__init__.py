@@ -53,7 +53,7 @@ class vpl_gen_info(C.Structure):
 
 COUNTER_NAMES = ["pairs", "traced", "visible", "box_tests", "tri_tests", "warp_rays", "warp_steps", "cone_tests",
                  "cone_packets", "ray_packets", "cache_hits", "cache_tests", "cand_lists", "cand_entries", "cand_fails",
-                 "filter_steps", "cand_steps", "filter_mt", "filter_mt_hits"]
+                 "filter_steps", "cand_steps", "filter_mt", "filter_mt_hits", "plane_culled"]
 
 
 class vpl_counters(C.Structure):

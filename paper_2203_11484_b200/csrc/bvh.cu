@@ -561,7 +561,7 @@ __global__ void k_wide4_write(const int* __restrict__ F, int nF, const int* __re
 
 
 __global__ void k_emit_tris(const float* __restrict__ verts, const uint32_t* __restrict__ sidx, int64_t n,
-                            const int* __restrict__ off, float4* __restrict__ tris) {
+                            const int* __restrict__ off, float4* __restrict__ tris, float4* __restrict__ planes) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= n) return;
     uint32_t t = sidx[p];
@@ -571,6 +571,15 @@ __global__ void k_emit_tris(const float* __restrict__ verts, const uint32_t* __r
     tris[3 * slot + 0] = make_float4(v0.x, v0.y, v0.z, __int_as_float((int)t));
     tris[3 * slot + 1] = make_float4(e1.x, e1.y, e1.z, 0.0f);
     tris[3 * slot + 2] = make_float4(e2.x, e2.y, e2.z, 0.0f);
+    // plane of the triangle MT sees, (v0, v0 + e1, v0 + e2), in float64 and rounded once: unit normal
+    // n and offset n.v0 (the gather's plane-side cull evaluates f(p) = n.p - offset; a zero-area
+    // triangle gets the null plane, which never culls)
+    const double nx = (double)e1.y * e2.z - (double)e1.z * e2.y, ny = (double)e1.z * e2.x - (double)e1.x * e2.z,
+                 nz = (double)e1.x * e2.y - (double)e1.y * e2.x;
+    const double len = sqrt(nx * nx + ny * ny + nz * nz);
+    const double il = len > 0.0 ? 1.0 / len : 0.0;
+    planes[slot] = make_float4((float)(nx * il), (float)(ny * il), (float)(nz * il),
+                               (float)((nx * v0.x + ny * v0.y + nz * v0.z) * il));
 }
 
 struct BuildWork {
@@ -768,7 +777,7 @@ int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* 
             }
         }
     }
-    k_emit_tris<<<nblk(n, 256), 256, 0, s>>>(sv.verts, w.idx2, n, w.off, tris);
+    k_emit_tris<<<nblk(n, 256), 256, 0, s>>>(sv.verts, w.idx2, n, w.off, tris, (float4*)((char*)d_bvh + bh.off_planes));
     VPL_LAUNCHED("k_emit_tris");
     if (n > 1) {
         int depth = 0;

@@ -107,7 +107,8 @@ inline SceneView scene_view(const void* blob, int64_t n) {
 }
 
 // BVH blob = BvhHdr, internal nodes (4 float4 each), leaf-ordered triangles
-// (3 float4 each: v0 | orig index bits, e1, e2).
+// (3 float4 each: v0 | orig index bits, e1, e2), leaf-ordered triangle planes
+// (1 float4 each: unit normal of e1 x e2 and offset n.v0, rounded from float64).
 // Two wide node formats built from the binary PLOC tree:
 //  * 4-wide (per-ray packet traversal): SoA child boxes as centre / half
 //    extent c.x[4] e.x[4] c.y[4] e.y[4] c.z[4] e.z[4], refs[4], meta (axis,
@@ -124,13 +125,14 @@ struct BvhHdr {
     int64_t n;
     int32_t root;       // 0 (internal) or ~0 (single leaf)
     int32_t pad;
-    int64_t off_nodes, off_tris, off_wide, off_wide4;
+    int64_t off_nodes, off_tris, off_wide, off_wide4, off_planes;
 };
 struct BvhView {
     const float4* nodes;   // binary nodes (per-thread traversals)
     const float4* tris;
     const float4* wide;    // 16-wide nodes (cone traversal)
     const float4* wide4;   // 4-wide nodes (per-ray packet traversal)
+    const float4* planes;  // leaf-ordered triangle planes (unit normal, offset): the gather's plane-side cull
     int32_t root;
     int32_t n;             // triangles (bounds checks under VPL_DEBUG)
     float box_pad;         // the scene's box padding (SceneHdr::box_pad), set by callers that need it
@@ -142,9 +144,10 @@ inline size_t bvh_layout(int64_t n, BvhHdr* h) {
     size_t o_t = off; off = align_up(off + sizeof(float4) * 3 * (size_t)n);
     size_t o_w = off; off = align_up(off + sizeof(float4) * kWideF4 * ni);
     size_t o_w4 = off; off = align_up(off + sizeof(float4) * kWide4F4 * ni);
+    size_t o_pl = off; off = align_up(off + sizeof(float4) * (size_t)n);
     if (h) {
         h->n = n; h->root = n > 1 ? 0 : ~0;
-        h->off_nodes = o_n; h->off_tris = o_t; h->off_wide = o_w; h->off_wide4 = o_w4;
+        h->off_nodes = o_n; h->off_tris = o_t; h->off_wide = o_w; h->off_wide4 = o_w4; h->off_planes = o_pl;
     }
     return off;
 }
@@ -156,6 +159,7 @@ inline BvhView bvh_view(const void* blob, int64_t n) {
     v.tris = (const float4*)((const char*)blob + h.off_tris);
     v.wide = (const float4*)((const char*)blob + h.off_wide);
     v.wide4 = (const float4*)((const char*)blob + h.off_wide4);
+    v.planes = (const float4*)((const char*)blob + h.off_planes);
     v.root = h.root;
     v.n = (int32_t)n;
     v.box_pad = 0.0f;
@@ -321,7 +325,7 @@ struct TravStats {
     uint32_t lists = 0, entries = 0, lfail = 0;       // cluster candidate lists built / their entries / unusable
     uint32_t fsteps = 0;                              // candidate-filter iterations (32 candidates each)
     uint32_t lsteps = 0;                              // traversal steps spent building candidate lists
-    uint32_t ftests = 0;                              // frustum pre-tests of list triangles (lane-level)
+    uint32_t pculled = 0;                             // box-hit triangles dropped by the plane-side cull (lane-level)
     uint32_t fmt = 0, fmt_hit = 0;                    // filter MT tests (warp-level) / those with a hit
 };
 

@@ -79,6 +79,17 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+// L1 prefetch of a triangle's three float4 (48 B, 16-byte aligned: at most two 32-byte sectors apart):
+// the lane that finds a box hit issues it, so the serial MT loop that follows finds the data in L1
+#ifndef VPL_TRI_PREFETCH
+#define VPL_TRI_PREFETCH 0   // measured: C4 753 -> 760 ms, C3 247 -> 251 ms (more L1 requests than the latency they hide)
+#endif
+__device__ __forceinline__ void prefetch_tri(const float4* tr) {
+#if VPL_TRI_PREFETCH
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(tr));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(tr + 2));
+#endif
+}
 __device__ __forceinline__ float sqrt_approx(float x) {
     float r;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -89,7 +100,58 @@ struct Beam {
     float a0[3], b0[3], a1[3], b1[3];
     float s_lo, s_hi;
     unsigned pos;   // bit a: D_a > 0
+    float y[3], dc[3], de[3];   // per-VPL beams: the VPL y, centre / half extent of the D box (plane_cull)
 };
+
+// Plane-side cull of a candidate triangle before its exact MT tests.  f(p) = n.p - o is the signed
+// distance from the triangle's plane (unit normal, BvhView::planes).  For the VPL, a = f(y); for the
+// receivers of the pending segments, x = y + D with D in the beam's D box, f(x) in [b_lo, b_hi] =
+// a + n.Dc -+ |n|.De.  Both ranges are widened by mu (the scene's box padding, ~100x the fp32 rounding
+// of f).  A segment x -> y can only be hit (O9: t in (eps, L - eps)) if it crosses the plane there:
+//   * a and every b on the same side: no crossing;
+//   * a > 0, some b < 0: the crossing is at t* = L|b| / (|b| + a) <= Lmax|b_lo| / a, below eps/2 when
+//     b_lo >= -s a with s = (eps/2) / Lmax (= Beam::s_lo): MT's t (error ~1e-7 |x - v0| / cos, and the
+//     condition forces cos >= 2 mu / eps) stays below eps — receivers lying on the triangle's own plane;
+//   * every b > 0, a < 0: likewise L - t* <= Lmax|a| / b_lo <= eps/2 — the VPL's own surface;
+// and the mirrored cases.  Such a triangle cannot produce an O9 hit for any pending segment, so
+// skipping its MT tests leaves every visibility bit unchanged.
+#ifndef VPL_PLANE_CULL
+#define VPL_PLANE_CULL 1
+#endif
+#ifndef VPL_PLANE_CULL_FILTER
+#define VPL_PLANE_CULL_FILTER 1   // per-VPL cull of list entries before their MT tests
+#endif
+#ifndef VPL_PLANE_CULL_TRAV
+#define VPL_PLANE_CULL_TRAV 0     // per-VPL cull of triangle children in the beam traversal (measured: C4 +26 ms, off)
+#endif
+__device__ __forceinline__ bool plane_cull(const Beam& B, float mu, float4 pl) {
+    const float a = fmaf(pl.x, B.y[0], fmaf(pl.y, B.y[1], fmaf(pl.z, B.y[2], -pl.w)));
+    const float c = fmaf(pl.x, B.dc[0], fmaf(pl.y, B.dc[1], pl.z * B.dc[2]));
+    const float e = fmaf(fabsf(pl.x), B.de[0], fmaf(fabsf(pl.y), B.de[1], fmaf(fabsf(pl.z), B.de[2], mu + mu)));
+    const float a_lo = a - mu, a_hi = a + mu;
+    const float b_lo = (a + c) - e, b_hi = (a + c) + e;
+    const float s = B.s_lo;
+    const bool pos = (fmaxf(a_lo, b_lo) > 0.0f) & (fmaf(s, a_lo, b_lo) >= 0.0f) & (fmaf(s, b_lo, a_lo) >= 0.0f);
+    const bool neg = (fminf(a_hi, b_hi) < 0.0f) & (fmaf(s, a_hi, b_hi) <= 0.0f) & (fmaf(s, b_hi, a_hi) <= 0.0f);
+    return pos | neg;
+}
+// the same cull for a run beam: y ranges over the run's position box (centre yc, half extent ye),
+// x over the participating receivers' box (xc, xe); s = (eps/2) / Lmax of the run beam
+#ifndef VPL_PLANE_CULL_RUN
+#define VPL_PLANE_CULL_RUN 0   // measured: shorter lists, but the test inside every build step costs more (C4 +47 ms): off
+#endif
+__device__ __forceinline__ bool plane_cull_run(const float* yc, const float* ye, const float* xc, const float* xe,
+                                               float s, float mu, float4 pl) {
+    const float ax = fabsf(pl.x), ay = fabsf(pl.y), az = fabsf(pl.z);
+    const float a = fmaf(pl.x, yc[0], fmaf(pl.y, yc[1], fmaf(pl.z, yc[2], -pl.w)));
+    const float b = fmaf(pl.x, xc[0], fmaf(pl.y, xc[1], fmaf(pl.z, xc[2], -pl.w)));
+    const float ea = fmaf(ax, ye[0], fmaf(ay, ye[1], fmaf(az, ye[2], mu)));
+    const float eb = fmaf(ax, xe[0], fmaf(ay, xe[1], fmaf(az, xe[2], mu)));
+    const float a_lo = a - ea, a_hi = a + ea, b_lo = b - eb, b_hi = b + eb;
+    const bool pos = (fmaxf(a_lo, b_lo) > 0.0f) & (fmaf(s, a_lo, b_lo) >= 0.0f) & (fmaf(s, b_lo, a_lo) >= 0.0f);
+    const bool neg = (fminf(a_hi, b_hi) < 0.0f) & (fmaf(s, a_hi, b_hi) <= 0.0f) & (fmaf(s, b_hi, a_hi) <= 0.0f);
+    return pos | neg;
+}
 
 __device__ __forceinline__ bool beam_from_bounds(const float* Dn, const float* Dm, const float* yl, const float* yh,
                                                  float lmin, float lmax, float spread_tol, float eps, Beam& B);
@@ -194,6 +256,12 @@ __device__ __forceinline__ bool make_beam(const Segs& S, f3 y, float eps, Beam& 
     const float lmin = sqrt_approx(warp_min_f32(l2n));
     const float lmax = sqrt_approx(warp_max_f32(l2m));
     const float yv[3] = {y.x, y.y, y.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        B.y[a] = yv[a];
+        B.dc[a] = 0.5f * (Dn[a] + Dm[a]);
+        B.de[a] = 0.5f * (Dm[a] - Dn[a]) + 2e-7f * fmaxf(fabsf(Dn[a]), fabsf(Dm[a]));   // |D - Dc| <= De incl. rounding
+    }
     return beam_from_bounds(Dn, Dm, yv, yv, lmin, lmax, kConeSpread, eps, B);
 }
 
@@ -339,7 +407,14 @@ __device__ __forceinline__ void beam_traverse(const BvhView& bv, Segs& S, float 
             if (lane == 0) st->cones += __popc(real);
         }
         const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
-        unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
+        bool leaf = hit && ref < 0;
+        if (VPL_PLANE_CULL && VPL_PLANE_CULL_TRAV && bv.planes && leaf) {
+            const bool cull = plane_cull(B, bv.box_pad, __ldg(bv.planes + (~ref >> 3)));
+            if (kCount && cull) st->pculled += 1;
+            leaf = !cull;
+        }
+        if (leaf) prefetch_tri(bv.tris + 3 * (~ref >> 3));
+        unsigned Bl = __ballot_sync(0xFFFFFFFFu, leaf);
         if (Bi) {
             const int nB = __popc(Bi >> 16), nA = __popc(Bi & 0xFFFFu);
             const int rank = __popc(Bi & below & hmask);
@@ -402,6 +477,13 @@ int build_cands(const BvhView& bv, const float* xl, const float* xh, const vpl_r
     yhi.x = warp_max_f32(yhi.x); yhi.y = warp_max_f32(yhi.y); yhi.z = warp_max_f32(yhi.z);
     ClusterBeam CB;
     if (!make_cluster_beam(xl, xh, ylo, yhi, eps, CB)) return -1;
+    // centre / half extent of the run box and the receivers' box (half extents rounded up)
+    const float yc[3] = {0.5f * (ylo.x + yhi.x), 0.5f * (ylo.y + yhi.y), 0.5f * (ylo.z + yhi.z)};
+    const float xc[3] = {0.5f * (xl[0] + xh[0]), 0.5f * (xl[1] + xh[1]), 0.5f * (xl[2] + xh[2])};
+    const float ye[3] = {fmaxf(yhi.x - yc[0], yc[0] - ylo.x) * 1.000001f, fmaxf(yhi.y - yc[1], yc[1] - ylo.y) * 1.000001f,
+                         fmaxf(yhi.z - yc[2], yc[2] - ylo.z) * 1.000001f};
+    const float xe[3] = {fmaxf(xh[0] - xc[0], xc[0] - xl[0]) * 1.000001f, fmaxf(xh[1] - xc[1], xc[1] - xl[1]) * 1.000001f,
+                         fmaxf(xh[2] - xc[2], xc[2] - xl[2]) * 1.000001f};
     const int half = lane >> 4;
     const unsigned below = (1u << lane) - 1u;
     if (lane == 0) sstack[0] = bv.root;
@@ -423,12 +505,15 @@ int build_cands(const BvhView& bv, const float* xl, const float* xh, const vpl_r
             if (lane == 0) st->cones += __popc(real);
         }
         const unsigned Bi = __ballot_sync(0xFFFFFFFFu, hit && ref >= 0);
-        const unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit && ref < 0);
+        bool leaf = hit && ref < 0;
+        if (VPL_PLANE_CULL && VPL_PLANE_CULL_RUN && bv.planes && leaf)
+            leaf = !plane_cull_run(yc, ye, xc, xe, CB.B.s_lo, bv.box_pad, __ldg(bv.planes + (~ref >> 3)));
+        const unsigned Bl = __ballot_sync(0xFFFFFFFFu, leaf);
         __syncwarp();
         if (Bl) {
             const int nl = __popc(Bl);
             if (n + nl > kCandCap) return -1;
-            if (hit && ref < 0) sstack[kWarpStack - 1 - (n + __popc(Bl & below))] = slot;
+            if (leaf) sstack[kWarpStack - 1 - (n + __popc(Bl & below))] = slot;
             n += nl;
         }
         if (Bi) {
@@ -456,10 +541,17 @@ __device__ __forceinline__ void filter_cands(const BvhView& bv, Segs& S, float t
         const int slot = ok ? sstack[kWarpStack - 1 - i] : 0;   // slot 0: a real child, masked below
         const float4* nd = (const float4*)((const char*)bv.wide + ((size_t)slot << 5));
         const float4 lo = __ldg(nd), hi = __ldg(nd + 1);
-        const bool hit = ok & beam_box(B, lo, hi);
+        bool hit = ok & beam_box(B, lo, hi);
         if (kCount && lane == 0) { st->fsteps += 1; st->cones += min(32, ncand - base); }
+        const int tri = ok ? ~__float_as_int(lo.w) >> 3 : 0;
+        if (VPL_PLANE_CULL && VPL_PLANE_CULL_FILTER && bv.planes) {
+            const bool cull = plane_cull(B, bv.box_pad, __ldg(bv.planes + tri));
+            if (kCount && hit && cull) st->pculled += 1;
+            hit &= !cull;
+        }
         unsigned Bl = __ballot_sync(0xFFFFFFFFu, hit);
-        const int toff = 3 * (~__float_as_int(lo.w) >> 3);   // float4 offset of the candidate's triangle
+        const int toff = 3 * tri;   // float4 offset of the candidate's triangle
+        if (hit) prefetch_tri(bv.tris + toff);
         while (Bl) {
             const int k = 31 - __clz(Bl);                      // highest first: one FLO
             Bl &= ~(1u << k);
@@ -479,6 +571,35 @@ __device__ __forceinline__ void filter_cands(const BvhView& bv, Segs& S, float t
     }
 }
 
+// Per-ray packet of one receiver slot (loose beams, ~1% of the packets): kept out of line so that its
+// code is not duplicated per slot inside the hot loop (instruction-cache footprint).  Returns the
+// occluding triangle of this lane's segment, or -1.
+#ifndef VPL_RAY_NOINLINE
+#define VPL_RAY_NOINLINE 0   // measured: C3 -1.6%, C4 +1.8%
+#endif
+template <bool kCount>
+#if VPL_RAY_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+int ray_packet(const BvhView& bv, f3 o, f3 d, float eps, float tmax, bool live, int* __restrict__ sstack,
+               TravStats* st) {
+    Ray r;
+    r.o = o; r.d = d; r.tmin = eps; r.tmax = tmax;
+    const unsigned lm = __ballot_sync(0xFFFFFFFFu, live);
+    const int leader = __ffs(lm) - 1;
+    const unsigned neg = (d.x < 0.0f ? 1u : 0u) | (d.y < 0.0f ? 2u : 0u) | (d.z < 0.0f ? 4u : 0u);
+    const unsigned dn = __shfl_sync(0xFFFFFFFFu, neg, leader);
+    OccluderCache c;
+    const bool occ = warp_traverse_ray<kCount>(bv, r, live, false, c, dn, sstack, st);
+    return occ && live ? c.own0 : -1;
+}
+
+#ifndef VPL_LIST_FIRST
+#define VPL_LIST_FIRST 1   // 1: the run list is looked up before the VPL's beam is made (an empty list needs no beam; a list
+                           // also serves loose beams); 0: beam first, lists only for tight beams
+#endif
 // Resolve the pending segments of one VPL y: the run's candidate list or a beam traversal, else
 // (loose beam) one per-ray packet per receiver slot.  part: bit k set if receiver k may trace the
 // current VPL cluster (render.cu's conservative cluster cull); xl / xh of the run beam are the box of
@@ -494,24 +615,40 @@ __device__ __forceinline__ void resolve(const BvhView& bv, Segs& S, float eps, f
     // the run list covers the participating receivers only (the cluster cull is conservative, so a
     // pending segment always belongs to one; checked anyway)
     const bool covered = !__any_sync(0xFFFFFFFFu, (S.pend & ~part) != 0);
-    if (make_beam(S, y, eps, B)) {
-        if (kCount && lane == 0) st->cpk += 1;
-        if (VPL_CANDS && i >= cand_end) {
-            const float inf = __int_as_float(0x7f800000);
-            float l[3] = {inf, inf, inf}, h[3] = {-inf, -inf, -inf};
+#if !VPL_LIST_FIRST
+    bool tight = make_beam(S, y, eps, B);
+    if (VPL_CANDS && tight && i >= cand_end) {
+#else
+    bool tight = false;
+    if (VPL_CANDS && i >= cand_end) {
+#endif
+        const float inf = __int_as_float(0x7f800000);
+        float l[3] = {inf, inf, inf}, h[3] = {-inf, -inf, -inf};
 #pragma unroll
-            for (int k = 0; k < kSeg; ++k)
-                if (part & (1u << k)) {
-                    l[0] = fminf(l[0], xr[k].x); l[1] = fminf(l[1], xr[k].y); l[2] = fminf(l[2], xr[k].z);
-                    h[0] = fmaxf(h[0], xr[k].x); h[1] = fmaxf(h[1], xr[k].y); h[2] = fmaxf(h[2], xr[k].z);
-                }
-            const float xl[3] = {warp_min_f32(l[0]), warp_min_f32(l[1]), warp_min_f32(l[2])};
-            const float xh[3] = {warp_max_f32(h[0]), warp_max_f32(h[1]), warp_max_f32(h[2])};
-            cand_end = min(i + VPL_CAND_GROUP, cend);
-            cand = build_cands<kCount>(bv, xl, xh, vpls + i, cand_end - i, eps, sstack, st);
-            if (kCount && lane == 0) { if (cand >= 0) { st->lists += 1; st->entries += cand; } else st->lfail += 1; }
-        }
-        if (VPL_CANDS && covered && cand >= 0)
+        for (int k = 0; k < kSeg; ++k)
+            if (part & (1u << k)) {
+                l[0] = fminf(l[0], xr[k].x); l[1] = fminf(l[1], xr[k].y); l[2] = fminf(l[2], xr[k].z);
+                h[0] = fmaxf(h[0], xr[k].x); h[1] = fmaxf(h[1], xr[k].y); h[2] = fmaxf(h[2], xr[k].z);
+            }
+        const float xl[3] = {warp_min_f32(l[0]), warp_min_f32(l[1]), warp_min_f32(l[2])};
+        const float xh[3] = {warp_max_f32(h[0]), warp_max_f32(h[1]), warp_max_f32(h[2])};
+        cand_end = min(i + VPL_CAND_GROUP, cend);
+        cand = build_cands<kCount>(bv, xl, xh, vpls + i, cand_end - i, eps, sstack, st);
+        if (kCount && lane == 0) { if (cand >= 0) { st->lists += 1; st->entries += cand; } else st->lfail += 1; }
+    }
+    const bool listed = VPL_CANDS && covered && cand >= 0;
+#if VPL_LIST_FIRST
+    if (listed && cand == 0) {   // nothing can block a segment of this run: every pending segment is visible
+        if (kCount && lane == 0) st->cpk += 1;
+        S.pend = 0;
+        return;
+    }
+    // (a list serves loose beams too: it holds every possible occluder of the run's segments)
+    tight = make_beam(S, y, eps, B) || listed;
+#endif
+    if (tight) {
+        if (kCount && lane == 0) st->cpk += 1;
+        if (listed)
             filter_cands<kCount>(bv, S, eps, B, sstack, cand, cache, st);
         else
             beam_traverse<kCount>(bv, S, eps, B, cache, sstack, st);
@@ -523,12 +660,8 @@ __device__ __forceinline__ void resolve(const BvhView& bv, Segs& S, float eps, f
             const unsigned lm = __ballot_sync(0xFFFFFFFFu, live);
             if (!lm) continue;                                          // uniform
             if (kCount && lane == 0) st->rpk += 1;
-            Ray r;
-            r.o = S.o[k]; r.d = S.d[k]; r.tmin = eps; r.tmax = S.tmax[k];
-            const int leader = __ffs(lm) - 1;
-            const unsigned neg = (r.d.x < 0.0f ? 1u : 0u) | (r.d.y < 0.0f ? 2u : 0u) | (r.d.z < 0.0f ? 4u : 0u);
-            const unsigned dn = __shfl_sync(0xFFFFFFFFu, neg, leader);
-            if (warp_traverse_ray<kCount>(bv, r, live, false, cache[k], dn, sstack, st) && live) S.occ |= 1u << k;
+            const int tri = ray_packet<kCount>(bv, S.o[k], S.d[k], eps, S.tmax[k], live, sstack, st);
+            if (tri >= 0) { S.occ |= 1u << k; cache[k].found(tri); }
         }
     }
     S.pend = 0;
@@ -549,31 +682,44 @@ __device__ __forceinline__ void cache_tests(const BvhView& bv, Segs& S, float ep
         test_tri<kCount, k, k + 1>(bv, S, S.pend & m, eps, cache[k].own1, cache, st);
 }
 
+#ifndef VPL_TWO_PASS
+#define VPL_TWO_PASS 1   // leave after the cosine tests when no receiver of the warp traces the VPL
+#endif
 // One VPL (position y, triangle yt; uniform) for one lane's receivers: Eq. 1 terms (O13, exact fp32
 // order), segment setup (O9), occluder caches, resolution.  act: bit k = receiver k is a front-face
-// hit.  Returns traced | vis << 16 (bit k per receiver) and w[k] = cx*ci / (r2 * max(r2, b2)).
+// hit; nb: the VPL's normal record (loaded by the caller, one VPL ahead).  Returns traced | vis << 16
+// (bit k per receiver) and w[k] = cx*ci / (r2 * max(r2, b2)).
 template <bool kCount>
 __device__ __forceinline__ unsigned shade(const BvhView& bv, const vpl_record* __restrict__ vpls, int i, f3 y, int yt,
-                                          const f3* xr, const f3* nr, const int* tri_x, unsigned act, float eps,
+                                          float4 nb, const f3* xr, const f3* nr, const int* tri_x, unsigned act, float eps,
                                           float b2, OccluderCache* cache, int* __restrict__ sstack, TravStats* st,
                                           float* w, int& cand, int& cand_end, int cend, unsigned part) {
-    Segs S;
-    S.pend = 0; S.occ = 0;
+    // pass 1: the cosine tests only (most VPLs are traced by no receiver of the warp: nothing else is
+    // computed or stored for them)
     unsigned traced = 0;
-    const float4 nb = __ldg((const float4*)(vpls + i) + 1);
 #pragma unroll
     for (int k = 0; k < kSeg; ++k) {
-        w[k] = 0.0f;
+        const f3 d = y - xr[k];
+        const float cx = dot_fma(nr[k], d);          // R26: the cosine terms as fused dots
+        const float ci = -dot_fma(xyz(nb), d);
+        w[k] = cx * ci;
+        if (((act >> k) & 1u) && yt != tri_x[k] && cx > 0.0f && ci > 0.0f) traced |= 1u << k;
+    }
+#if VPL_TWO_PASS
+    if (!__any_sync(0xFFFFFFFFu, traced != 0)) return 0;
+#endif
+    // pass 2: Eq. 1 weight and segment setup of the traced receivers
+    Segs S;
+    S.pend = 0; S.occ = 0;
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) {
         S.o[k] = xr[k];
         S.d[k] = mk3(0.0f, 0.0f, 0.0f);
         S.tmax[k] = 0.0f;
-        const f3 d = y - xr[k];
-        const float r2 = dot(d, d);
-        const float cx = dot_fma(nr[k], d);          // R26: the cosine terms as fused dots
-        const float ci = -dot_fma(xyz(nb), d);
-        if (((act >> k) & 1u) && yt != tri_x[k] && cx > 0.0f && ci > 0.0f) {
-            traced |= 1u << k;
-            w[k] = (cx * ci) * rcp_approx(r2 * fmaxf(r2, b2));   // r2 * max(r2, b2) >= b2^2: normal range
+        if (traced & (1u << k)) {
+            const f3 d = y - xr[k];
+            const float r2 = dot(d, d);
+            w[k] = w[k] * rcp_approx(r2 * fmaxf(r2, b2));   // (cx * ci) / ...; r2 * max(r2, b2) >= b2^2: normal range
 #if VPL_FAST_SEG
             // one MUFU: 1/dist and dist within ~2 ulp of O9's IEEE sqrt / division (visibility then
             // differs from the oracle only for grazing hits, inside BJ:5's 1e-4 budget; reading R28)
@@ -589,7 +735,9 @@ __device__ __forceinline__ unsigned shade(const BvhView& bv, const vpl_record* _
             if (S.tmax[k] > eps) S.pend |= 1u << k;
         }
     }
+#if !VPL_TWO_PASS
     if (!__any_sync(0xFFFFFFFFu, traced != 0)) return 0;
+#endif
     // occluder caches: exact MT of each receiver's segment against its recent occluders; a receiver
     // whose last traced segment was visible skips its cache (visibility is coherent along the
     // spatially ordered VPLs)

@@ -80,6 +80,15 @@ __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, floa
 #ifndef VPL_GATHER_CTAS
 #define VPL_GATHER_CTAS 32
 #endif
+#ifndef VPL_PREFETCH_VPL
+#define VPL_PREFETCH_VPL 0   // load each VPL's position / normal records one iteration ahead (measured: 8 more live
+                             // registers cost C4 762 -> 828 ms, C3 252 -> 265 ms: off)
+#endif
+#ifndef VPL_TAIL_BLOCKS
+#define VPL_TAIL_BLOCKS -1  // >= 0: whole-block tasks for all but the last VPL_TAIL_BLOCKS x grid blocks of a call (no partial
+                            // sums for them); measured at 2: block costs vary ~10x, the long tasks unbalance the SMs (C3 226 ->
+                            // 496 ms, C4 670 -> 807 ms); -1: (block, chunk) tasks only (whole-block only when M fits one chunk)
+#endif
 #ifndef VPL_PART_EVICT_LAST
 #define VPL_PART_EVICT_LAST 1   // partial stores with an L2 evict_last policy (C4: DRAM writes 120 -> 64 MB per launch)
 #endif
@@ -98,29 +107,35 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                                                 vpl_counters* __restrict__ ctr, int* __restrict__ queue,
                                                 const float4* __restrict__ clusters, int32_t chunk, int32_t n_chunks,
                                                 float* __restrict__ part_out, int* __restrict__ done,
-                                                int* __restrict__ slot_gen, int32_t ring, GatherDump dump) {
+                                                int* __restrict__ slot_gen, int32_t ring, int32_t n_whole,
+                                                GatherDump dump) {
     __shared__ int sstack[kWarpStack];
     __shared__ float s_acc[kSeg][3][32];   // running per-receiver totals (kept out of the register budget)
+    __shared__ float s_tot[kSeg][3][32];   // whole-block tasks: the chunk totals folded in chunk order
     constexpr int kPart = 96 * kSeg;       // partial floats per (block, chunk): 32 lanes x kSeg receivers x 3
     const int lane = threadIdx.x;
-    const int64_t ntask = tm.n_warps() * n_chunks;
+    // Tasks: the first n_whole blocks of the call are whole-block tasks (one warp walks all the chunks of
+    // the block and folds their totals in chunk order itself: no partial sums leave the SM); the
+    // remaining blocks are split into (block, chunk) tasks, fine-grained enough that the dynamic queue
+    // balances the SMs at the end of the launch and when a rank holds 1/8 of the frame.  Both give the
+    // same fp32 sums: chunk totals from zero, folded in chunk order.
+    const int64_t ntask = n_whole + (tm.n_warps() - n_whole) * n_chunks;
     const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
     while (true) {
         int64_t g;
         if (lane == 0) g = atomicAdd(queue, 1);
         g = __shfl_sync(0xFFFFFFFFu, g, 0);
         if (g >= ntask) break;
-        // task = (8 x 4kSeg pixel block, VPL chunk): fine-grained enough that the dynamic queue balances
-        // the SMs even when a rank holds 1/8 of the frame
-        const int ch = (int)(g % n_chunks);
-        const int vbeg = ch * chunk, vend = min(M, vbeg + chunk);
+        const bool whole = g < n_whole;
+        const int64_t blk = whole ? g : n_whole + (g - n_whole) / n_chunks;   // 8 x 4kSeg pixel block of the call
+        const int ch0 = whole ? 0 : (int)((g - n_whole) % n_chunks), ch1 = whole ? n_chunks : ch0 + 1;
         int32_t pix[kSeg];
         f3 x[kSeg], nx[kSeg];
         int tri_x[kSeg];
         unsigned act = 0;
 #pragma unroll
         for (int k = 0; k < kSeg; ++k) {
-            pix[k] = tm.pixel(g / n_chunks, lane, k);
+            pix[k] = tm.pixel(blk, lane, k);
             x[k] = mk3(0, 0, 0); nx[k] = mk3(0, 0, 0);
             tri_x[k] = -1;
             if (pix[k] >= 0) {
@@ -130,11 +145,16 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 if (tri_x[k] >= 0 && __float_as_int(b.w) != 0) act |= 1u << k;
                 x[k] = xyz(a); nx[k] = xyz(b);
             }
-            s_acc[k][0][lane] = 0.0f; s_acc[k][1][lane] = 0.0f; s_acc[k][2][lane] = 0.0f;
+            s_tot[k][0][lane] = 0.0f; s_tot[k][1][lane] = 0.0f; s_tot[k][2][lane] = 0.0f;
         }
         OccluderCache cache[kSeg];
         TravStats st;
-        unsigned long long n_traced = 0, n_vis = 0;
+        unsigned long long n_traced = 0, n_vis = 0, n_pairs = 0;
+        for (int ch = ch0; ch < ch1; ++ch) {
+        const int vbeg = ch * chunk, vend = min(M, vbeg + chunk);
+        if (kCount) n_pairs += (unsigned long long)__popc(act) * (unsigned long long)(vend - vbeg);
+#pragma unroll
+        for (int k = 0; k < kSeg; ++k) { s_acc[k][0][lane] = 0.0f; s_acc[k][1][lane] = 0.0f; s_acc[k][2][lane] = 0.0f; }
         if (__any_sync(0xFFFFFFFFu, act != 0)) {
             for (int i0 = vbeg; i0 < vend; i0 += 256) {
                 float part[kSeg][3];
@@ -150,10 +170,21 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                     if (cb && !__any_sync(0xFFFFFFFFu, inc != 0)) continue;   // no receiver can trace any VPL of it
                     const int c1 = min(c0 + kCluster, i1);
                     int cand = -1, cand_end = cb ? c0 : INT_MAX;           // candidate list (lazy) and its VPL range end
+#if VPL_PREFETCH_VPL
+                    float4 yv_n = __ldg((const float4*)(vpls + c0)), nb_n = __ldg((const float4*)(vpls + c0) + 1);
+#endif
                     for (int i = c0; i < c1; ++i) {
-                        const float4 yv = __ldg((const float4*)(vpls + i));
+#if VPL_PREFETCH_VPL
+                        // position / normal records one VPL ahead (the load latency overlaps this VPL's work)
+                        const float4 yv = yv_n, nb = nb_n;
+                        const int in = min(i + 1, M - 1);
+                        yv_n = __ldg((const float4*)(vpls + in));
+                        nb_n = __ldg((const float4*)(vpls + in) + 1);
+#else
+                        const float4 yv = __ldg((const float4*)(vpls + i)), nb = __ldg((const float4*)(vpls + i) + 1);
+#endif
                         float w[kSeg];
-                        const unsigned tv = shade<kCount>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), x, nx, tri_x, act,
+                        const unsigned tv = shade<kCount>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), nb, x, nx, tri_x, act,
                                                           eps, b2, cache, sstack, &st, w, cand, cand_end, c1, inc);
                         const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
                         if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
@@ -187,25 +218,33 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 }
             }
         }
+        if (whole) {   // the same fold as the chunked path's: totals from 0.0f, chunk totals added in chunk order
+#pragma unroll
+            for (int k = 0; k < kSeg; ++k) {
+                s_tot[k][0][lane] += s_acc[k][0][lane]; s_tot[k][1][lane] += s_acc[k][1][lane];
+                s_tot[k][2][lane] += s_acc[k][2][lane];
+            }
+        }
+        }   // chunks of the task
         const float sc = (float)(1.0 / kPiR);
-        if (n_chunks == 1) {
+        if (whole) {
 #pragma unroll
             for (int k = 0; k < kSeg; ++k)
                 if (pix[k] >= 0) {
                     const bool on = (act >> k) & 1u;
                     const f3 rho = xyz(((const float4*)(gb + pix[k]))[2]);
                     float* o = rgb + 3 * (int64_t)pix[k];
-                    o[0] = on ? s_acc[k][0][lane] * rho.x * sc : 0.0f;
-                    o[1] = on ? s_acc[k][1][lane] * rho.y * sc : 0.0f;
-                    o[2] = on ? s_acc[k][2][lane] * rho.z * sc : 0.0f;
+                    o[0] = on ? s_tot[k][0][lane] * rho.x * sc : 0.0f;
+                    o[1] = on ? s_tot[k][1][lane] * rho.y * sc : 0.0f;
+                    o[2] = on ? s_tot[k][2][lane] * rho.z * sc : 0.0f;
                 }
-        }
-        if (n_chunks > 1) {
+        } else {
+            const int ch = ch0;
             // chunk partial sums, (slot, chunk, receiver, lane)-contiguous in a ring of `ring` block slots
             // (the call's block ordinal modulo ring: a few MB stay L2-resident); the warp that completes a
             // block's last chunk folds them in chunk order (fp32), writes the pixels, discards the partial
             // lines (never written back to HBM) and hands the slot to the block `ring` later.
-            const int64_t lb = g / n_chunks;
+            const int64_t lb = blk - n_whole;
             const int slot = (int)(lb % ring), gen = (int)(lb / ring);
             float* pb = part_out + ((int64_t)slot * n_chunks) * kPart;
             if (lane == 0) {   // the slot's previous block (dispensed earlier, so running) must be folded
@@ -265,12 +304,11 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             }
         }
         if (kCount) {
-            unsigned long long pairs = (unsigned long long)__popc(act) * (unsigned long long)(vend - vbeg);
-            unsigned long long v[19] = {pairs, n_traced, n_vis, st.boxes, st.tris, st.wrays, st.wsteps,
+            unsigned long long v[20] = {n_pairs, n_traced, n_vis, st.boxes, st.tris, st.wrays, st.wsteps,
                                         st.cones, st.cpk, st.rpk, st.chits, st.ctests, st.lists, st.entries,
-                                        st.lfail, st.fsteps, st.lsteps, st.fmt, st.fmt_hit};
+                                        st.lfail, st.fsteps, st.lsteps, st.fmt, st.fmt_hit, st.pculled};
 #pragma unroll
-            for (int q = 0; q < 19; ++q) {
+            for (int q = 0; q < 20; ++q) {
                 unsigned long long a = v[q];
                 for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
                 if (lane == 0) atomicAdd(&ctr->pairs + q, a);
@@ -304,10 +342,10 @@ __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict
         uint32_t tb = 0, vb = 0;
         const int i0 = (int)(wd * 32), i1 = min(M, i0 + 32);
         for (int i = i0; i < i1; ++i) {
-            const float4 yv = __ldg((const float4*)(vpls + i));
+            const float4 yv = __ldg((const float4*)(vpls + i)), nb = __ldg((const float4*)(vpls + i) + 1);
             float w[kSeg];
             int cand = -1, cand_end = INT_MAX;
-            const unsigned tv = shade<false>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), x, nx, tri_x, act, eps, b2,
+            const unsigned tv = shade<false>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), nb, x, nx, tri_x, act, eps, b2,
                                              cache, sstack, nullptr, w, cand, cand_end, i1, act);
             tb |= (tv & 1u) << (i - i0);
             vb |= ((tv >> 16) & 1u) << (i - i0);
@@ -648,9 +686,16 @@ static int32_t gather_impl(const void* d_scene, const void* d_bvh, const vpl_gpo
     VPL_CUDA(cudaGetDevice(&dev));
     VPL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     int grid = sms * VPL_GATHER_CTAS;  // persistent: VPL_GATHER_CTAS one-warp CTAs per SM
+    // whole-block tasks for all but the last VPL_TAIL_BLOCKS x grid blocks of the call (the chunked tail balances
+    // the SMs; a rank with fewer blocks than that runs chunked tasks only, as does a dump run)
+    const int64_t nblk = tm.n_warps();
+    int64_t n_whole = n_chunks == 1 ? nblk : nblk - (int64_t)VPL_TAIL_BLOCKS * grid;
+    if (n_whole < 0 || (VPL_TAIL_BLOCKS < 0 && n_chunks > 1)) n_whole = 0;
+    if (n_whole > INT32_MAX) n_whole = INT32_MAX;
     SceneView sv = scene_view(d_scene, hh.n);
     BvhView bv = bvh_view(d_bvh, hh.n);
     bv.box_pad = hh.box_pad;
+    if (flags & VPL_GATHER_NO_CULL) bv.planes = nullptr;   // reference run: no cluster cull, no lists, no plane-side cull
 #ifdef VPL_CARVEOUT
     // shared-memory carveout preference (percent of the unified L1/shared array; tuning builds only)
     VPL_CUDA(cudaFuncSetAttribute(k_gather<false>, cudaFuncAttributePreferredSharedMemoryCarveout, VPL_CARVEOUT));
@@ -658,13 +703,13 @@ static int32_t gather_impl(const void* d_scene, const void* d_bvh, const vpl_gpo
 #endif
     if (dump.slot)
         k_gather<true, true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue, clusters, chunk,
-                                                  n_chunks, w.part, w.done, w.slot_gen, w.ring, dump);
+                                                  n_chunks, w.part, w.done, w.slot_gen, w.ring, (int32_t)n_whole, dump);
     else if (d_ctr)
         k_gather<true><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, d_ctr, queue, clusters, chunk,
-                                            n_chunks, w.part, w.done, w.slot_gen, w.ring, dump);
+                                            n_chunks, w.part, w.done, w.slot_gen, w.ring, (int32_t)n_whole, dump);
     else
         k_gather<false><<<grid, 32, 0, s>>>(sv, bv, tm, d_gbuf, vp, n_vpls, d_rgb, nullptr, queue, clusters, chunk,
-                                             n_chunks, w.part, w.done, w.slot_gen, w.ring, dump);
+                                             n_chunks, w.part, w.done, w.slot_gen, w.ring, (int32_t)n_whole, dump);
     VPL_LAUNCHED("k_gather");
 
     return VPL_OK;
@@ -738,8 +783,10 @@ int32_t vpl_visibility_dump(const void* d_scene, const void* d_bvh, const vpl_gp
     SceneHdr hh;
     VPL_TRY(read_scene_hdr(d_scene, s, &hh));
     if (n_pixels == 0) return VPL_OK;
-    k_visdump<<<nb(n_pixels, 64), 64, 0, s>>>(scene_view(d_scene, hh.n), bvh_view(d_bvh, hh.n), d_gbuf, d_vpls, n_vpls,
-                                           d_pixels, n_pixels, d_traced_bits, d_vis_bits);
+    BvhView bv = bvh_view(d_bvh, hh.n);
+    bv.box_pad = hh.box_pad;   // margin of the plane-side cull
+    k_visdump<<<nb(n_pixels, 64), 64, 0, s>>>(scene_view(d_scene, hh.n), bv, d_gbuf, d_vpls, n_vpls, d_pixels, n_pixels,
+                                           d_traced_bits, d_vis_bits);
     VPL_LAUNCHED("k_visdump");
     return VPL_OK;
 }

@@ -51,7 +51,7 @@ def test_library_is_sm100a_code(lib):
 
 
 def test_host_only_calls(lib):
-    assert lib.vpl_abi_version() == 3
+    assert lib.vpl_abi_version() == 4
     assert lib.vpl_status_string(0) == b"ok"
     assert lib.vpl_status_string(-2) == b"buffer too small"
     n = C.c_size_t()
