@@ -53,6 +53,25 @@ __device__ __forceinline__ bool cluster_may_trace(const float4* __restrict__ cb,
     const float m = 1e-4f * scale;   // >> the rounding of d = y - x and of the two dots
     return (ax + ay) + az > -m && (bx + by) + bz > -m;
 }
+// Can any receiver with position in [xl, xh] and normal in [nl, nh] (rb = xl nl xh nh) trace VPL v, i.e.
+// can cx = n_x.(y - x) > 0 and ci = n_y.(x - y) > 0 both hold?  Interval bounds per axis, with the
+// cluster cull's margin (far above the fp32 rounding of O13's dots).
+__device__ __forceinline__ bool vpl_may_trace(const vpl_record* __restrict__ v, const float* rb) {
+    const float4 yv = __ldg((const float4*)v), nv = __ldg((const float4*)v + 1);
+    const float y[3] = {yv.x, yv.y, yv.z}, ny[3] = {nv.x, nv.y, nv.z};
+    float cx = 0.0f, ci = 0.0f, sx = 0.0f, sy = 0.0f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float xl = rb[a], nl = rb[3 + a], xh = rb[6 + a], nh = rb[9 + a];
+        const float dl = y[a] - xh, dh = y[a] - xl;   // y - x over the box
+        cx += fmaxf(fmaxf(nl * dl, nl * dh), fmaxf(nh * dl, nh * dh));
+        ci += fmaxf(ny[a] * -dl, ny[a] * -dh);
+        sx = fmaxf(sx, fmaxf(fabsf(xl), fabsf(xh)));
+        sy = fmaxf(sy, fabsf(y[a]));
+    }
+    const float m = 1e-4f * (sx + sy);
+    return cx > -m && ci > -m;
+}
 __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, float4* __restrict__ cb) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;     // one thread per cluster
     if ((int64_t)c * kCluster >= M) return;
@@ -80,9 +99,8 @@ __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, floa
 #ifndef VPL_GATHER_CTAS
 #define VPL_GATHER_CTAS 32
 #endif
-#ifndef VPL_PREFETCH_VPL
-#define VPL_PREFETCH_VPL 0   // load each VPL's position / normal records one iteration ahead (measured: 8 more live
-                             // registers cost C4 762 -> 828 ms, C3 252 -> 265 ms: off)
+#ifndef VPL_VPL_CULL
+#define VPL_VPL_CULL 1   // per-VPL cull against the receiver block's bounds, one VPL per lane
 #endif
 #ifndef VPL_TAIL_BLOCKS
 #define VPL_TAIL_BLOCKS -1  // >= 0: whole-block tasks for all but the last VPL_TAIL_BLOCKS x grid blocks of a call (no partial
@@ -112,6 +130,7 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
     __shared__ int sstack[kWarpStack];
     __shared__ float s_acc[kSeg][3][32];   // running per-receiver totals (kept out of the register budget)
     __shared__ float s_tot[kSeg][3][32];   // whole-block tasks: the chunk totals folded in chunk order
+    __shared__ float s_rb[12];             // receiver bounds of the task: lo(x, n), hi(x, n)  (VPL_VPL_CULL)
     constexpr int kPart = 96 * kSeg;       // partial floats per (block, chunk): 32 lanes x kSeg receivers x 3
     const int lane = threadIdx.x;
     // Tasks: the first n_whole blocks of the call are whole-block tasks (one warp walks all the chunks of
@@ -147,6 +166,24 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             }
             s_tot[k][0][lane] = 0.0f; s_tot[k][1][lane] = 0.0f; s_tot[k][2][lane] = 0.0f;
         }
+        if (VPL_VPL_CULL) {   // bounds of the block's front-face receivers and of their normals (uniform)
+            const float inf = __int_as_float(0x7f800000);
+            float lo[6] = {inf, inf, inf, inf, inf, inf}, hi[6] = {-inf, -inf, -inf, -inf, -inf, -inf};
+#pragma unroll
+            for (int k = 0; k < kSeg; ++k)
+                if ((act >> k) & 1u) {
+                    const float v[6] = {x[k].x, x[k].y, x[k].z, nx[k].x, nx[k].y, nx[k].z};
+#pragma unroll
+                    for (int a = 0; a < 6; ++a) { lo[a] = fminf(lo[a], v[a]); hi[a] = fmaxf(hi[a], v[a]); }
+                }
+            __syncwarp();
+#pragma unroll
+            for (int a = 0; a < 6; ++a) {
+                const float l = warp_min_f32(lo[a]), h = warp_max_f32(hi[a]);
+                if (lane == 0) { s_rb[a] = l; s_rb[6 + a] = h; }
+            }
+            __syncwarp();
+        }
         OccluderCache cache[kSeg];
         TravStats st;
         unsigned long long n_traced = 0, n_vis = 0, n_pairs = 0;
@@ -170,19 +207,16 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                     if (cb && !__any_sync(0xFFFFFFFFu, inc != 0)) continue;   // no receiver can trace any VPL of it
                     const int c1 = min(c0 + kCluster, i1);
                     int cand = -1, cand_end = cb ? c0 : INT_MAX;           // candidate list (lazy) and its VPL range end
-#if VPL_PREFETCH_VPL
-                    float4 yv_n = __ldg((const float4*)(vpls + c0)), nb_n = __ldg((const float4*)(vpls + c0) + 1);
-#endif
-                    for (int i = c0; i < c1; ++i) {
-#if VPL_PREFETCH_VPL
-                        // position / normal records one VPL ahead (the load latency overlaps this VPL's work)
-                        const float4 yv = yv_n, nb = nb_n;
-                        const int in = min(i + 1, M - 1);
-                        yv_n = __ldg((const float4*)(vpls + in));
-                        nb_n = __ldg((const float4*)(vpls + in) + 1);
-#else
+                    // per-VPL cull, transposed: lane l tests VPL c0 + l against the box of the block's
+                    // receivers and the box of their normals (s_rb) — can cx > 0 and ci > 0 hold for any
+                    // of them?  Same conservative margin as the cluster cull; the VPL loop then visits
+                    // only the VPLs some receiver may trace.
+                    unsigned need = 0xFFFFFFFFu >> (32 - (c1 - c0));
+                    if (VPL_VPL_CULL && cb) need &= __ballot_sync(0xFFFFFFFFu, vpl_may_trace(vpls + min(c0 + lane, c1 - 1), s_rb));
+                    while (need) {
+                        const int i = c0 + __ffs(need) - 1;
+                        need &= need - 1u;
                         const float4 yv = __ldg((const float4*)(vpls + i)), nb = __ldg((const float4*)(vpls + i) + 1);
-#endif
                         float w[kSeg];
                         const unsigned tv = shade<kCount>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), nb, x, nx, tri_x, act,
                                                           eps, b2, cache, sstack, &st, w, cand, cand_end, c1, inc);
