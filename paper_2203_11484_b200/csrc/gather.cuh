@@ -96,12 +96,23 @@ __device__ __forceinline__ float sqrt_approx(float x) {
     return r;
 }
 
+#ifndef VPL_PLANE_SMEM
+#define VPL_PLANE_SMEM 0   // measured: spills 292 -> 268 B but C4 +0.5-2%: off
+#endif
 struct Beam {
     float a0[3], b0[3], a1[3], b1[3];
     float s_lo, s_hi;
     unsigned pos;   // bit a: D_a > 0
+#if !VPL_PLANE_SMEM
     float y[3], dc[3], de[3];   // per-VPL beams: the VPL y, centre / half extent of the D box (plane_cull)
+#endif
 };
+// (VPL_PLANE_SMEM: y, dc, de are uniform and only read at the head of a filter batch, so they live in
+// shared memory — 12 floats per warp — instead of 9 registers across the MT loops)
+__device__ __forceinline__ float* plane_terms() {
+    __shared__ __align__(16) float s_plane[2][12];   // [warp of the CTA (k_visdump runs two)][y dc de, padded]
+    return s_plane[(threadIdx.x >> 5) & 1];
+}
 
 // Plane-side cull of a candidate triangle before its exact MT tests.  f(p) = n.p - o is the signed
 // distance from the triangle's plane (unit normal, BvhView::planes).  For the VPL, a = f(y); for the
@@ -125,9 +136,17 @@ struct Beam {
 #define VPL_PLANE_CULL_TRAV 0     // per-VPL cull of triangle children in the beam traversal (measured: C4 +26 ms, off)
 #endif
 __device__ __forceinline__ bool plane_cull(const Beam& B, float mu, float4 pl) {
+#if VPL_PLANE_SMEM
+    const float4* sp = (const float4*)plane_terms();
+    const float4 Y = sp[0], DC = sp[1], DE = sp[2];
+    const float a = fmaf(pl.x, Y.x, fmaf(pl.y, Y.y, fmaf(pl.z, Y.z, -pl.w)));
+    const float c = fmaf(pl.x, DC.x, fmaf(pl.y, DC.y, pl.z * DC.z));
+    const float e = fmaf(fabsf(pl.x), DE.x, fmaf(fabsf(pl.y), DE.y, fmaf(fabsf(pl.z), DE.z, mu + mu)));
+#else
     const float a = fmaf(pl.x, B.y[0], fmaf(pl.y, B.y[1], fmaf(pl.z, B.y[2], -pl.w)));
     const float c = fmaf(pl.x, B.dc[0], fmaf(pl.y, B.dc[1], pl.z * B.dc[2]));
     const float e = fmaf(fabsf(pl.x), B.de[0], fmaf(fabsf(pl.y), B.de[1], fmaf(fabsf(pl.z), B.de[2], mu + mu)));
+#endif
     const float a_lo = a - mu, a_hi = a + mu;
     const float b_lo = (a + c) - e, b_hi = (a + c) + e;
     const float s = B.s_lo;
@@ -256,12 +275,27 @@ __device__ __forceinline__ bool make_beam(const Segs& S, f3 y, float eps, Beam& 
     const float lmin = sqrt_approx(warp_min_f32(l2n));
     const float lmax = sqrt_approx(warp_max_f32(l2m));
     const float yv[3] = {y.x, y.y, y.z};
+#if VPL_PLANE_SMEM
+    if (VPL_PLANE_CULL) {
+        float* sp = plane_terms();
+        __syncwarp();   // the previous beam's readers are done
+        if ((threadIdx.x & 31) < 3) {
+            const int a = threadIdx.x & 31;
+            const float dn = a == 0 ? Dn[0] : a == 1 ? Dn[1] : Dn[2], dm = a == 0 ? Dm[0] : a == 1 ? Dm[1] : Dm[2];
+            sp[a] = a == 0 ? yv[0] : a == 1 ? yv[1] : yv[2];
+            sp[4 + a] = 0.5f * (dn + dm);
+            sp[8 + a] = 0.5f * (dm - dn) + 2e-7f * fmaxf(fabsf(dn), fabsf(dm));   // |D - Dc| <= De incl. rounding
+        }
+        __syncwarp();
+    }
+#else
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         B.y[a] = yv[a];
         B.dc[a] = 0.5f * (Dn[a] + Dm[a]);
         B.de[a] = 0.5f * (Dm[a] - Dn[a]) + 2e-7f * fmaxf(fabsf(Dn[a]), fabsf(Dm[a]));   // |D - Dc| <= De incl. rounding
     }
+#endif
     return beam_from_bounds(Dn, Dm, yv, yv, lmin, lmax, kConeSpread, eps, B);
 }
 
@@ -682,6 +716,19 @@ __device__ __forceinline__ void cache_tests(const BvhView& bv, Segs& S, float ep
         test_tri<kCount, k, k + 1>(bv, S, S.pend & m, eps, cache[k].own1, cache, st);
 }
 
+// O13's cosine tests alone (the same operations as shade's first pass): bit k = receiver k traces the VPL
+__device__ __forceinline__ unsigned cosine_tests(f3 y, int yt, float4 nb, const f3* xr, const f3* nr, const int* tri_x,
+                                                 unsigned act) {
+    unsigned traced = 0;
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) {
+        const f3 d = y - xr[k];
+        const float cx = dot_fma(nr[k], d);
+        const float ci = -dot_fma(xyz(nb), d);
+        if (((act >> k) & 1u) && yt != tri_x[k] && cx > 0.0f && ci > 0.0f) traced |= 1u << k;
+    }
+    return traced;
+}
 #ifndef VPL_TWO_PASS
 #define VPL_TWO_PASS 1   // leave after the cosine tests when no receiver of the warp traces the VPL
 #endif

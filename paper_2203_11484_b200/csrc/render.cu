@@ -99,6 +99,25 @@ __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, floa
 #ifndef VPL_GATHER_CTAS
 #define VPL_GATHER_CTAS 32
 #endif
+#ifndef VPL_INTERLEAVE
+#define VPL_INTERLEAVE 1
+#endif
+#ifndef VPL_CHUNK_GROUP
+#define VPL_CHUNK_GROUP 128   // VPLs per interleave group (a multiple of the cluster size that divides 256); each group's
+                              // fp32 partial is folded into the chunk total
+#endif
+constexpr int kGroup = VPL_CHUNK_GROUP;
+static_assert(kGroup % kCluster == 0 && 256 % kGroup == 0, "interleave group");
+#ifndef VPL_NX_SMEM
+#define VPL_NX_SMEM 0
+#endif
+#ifndef VPL_SCAN_LOOP
+#define VPL_SCAN_LOOP 0   // inner loop over the VPLs no receiver of the warp traces (measured: C3 +3%, C4 +2%: off)
+#endif
+#ifndef VPL_ACC_SMEM
+#define VPL_ACC_SMEM 0   // 1: Eq. 1 sums accumulate in the shared-memory totals directly instead of 6 registers folded per
+                         // group (measured: spills 268 -> 220 B but C4 +1.7%: off)
+#endif
 #ifndef VPL_VPL_CULL
 #define VPL_VPL_CULL 1   // per-VPL cull against the receiver block's bounds, one VPL per lane
 #endif
@@ -129,8 +148,15 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                                                 GatherDump dump) {
     __shared__ int sstack[kWarpStack];
     __shared__ float s_acc[kSeg][3][32];   // running per-receiver totals (kept out of the register budget)
+#if VPL_TAIL_BLOCKS >= 0
     __shared__ float s_tot[kSeg][3][32];   // whole-block tasks: the chunk totals folded in chunk order
+#else
+    float (*s_tot)[3][32] = s_acc;         // whole-block tasks have a single chunk: its total is the block's
+#endif
     __shared__ float s_rb[12];             // receiver bounds of the task: lo(x, n), hi(x, n)  (VPL_VPL_CULL)
+#if VPL_NX_SMEM
+    __shared__ float4 s_nx[kSeg][32];      // receiver normal | triangle id
+#endif
     constexpr int kPart = 96 * kSeg;       // partial floats per (block, chunk): 32 lanes x kSeg receivers x 3
     const int lane = threadIdx.x;
     // Tasks: the first n_whole blocks of the call are whole-block tasks (one warp walks all the chunks of
@@ -164,8 +190,28 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 if (tri_x[k] >= 0 && __float_as_int(b.w) != 0) act |= 1u << k;
                 x[k] = xyz(a); nx[k] = xyz(b);
             }
+#if VPL_TAIL_BLOCKS >= 0
             s_tot[k][0][lane] = 0.0f; s_tot[k][1][lane] = 0.0f; s_tot[k][2][lane] = 0.0f;
+#endif
         }
+#if VPL_NX_SMEM
+        // receiver normals and triangle ids live in shared memory (one LDS.128 per receiver where they are
+        // used) instead of 8 registers that the 64-register cap turns into per-VPL local-memory reloads
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < kSeg; ++k) s_nx[k][lane] = make_float4(nx[k].x, nx[k].y, nx[k].z, __int_as_float(tri_x[k]));
+        __syncwarp();
+#define VPL_LOAD_NX()                                                          \
+        f3 nxl[kSeg];                                                          \
+        int tril[kSeg];                                                        \
+        _Pragma("unroll") for (int k = 0; k < kSeg; ++k) {                     \
+            const float4 q = s_nx[k][lane];                                    \
+            nxl[k] = xyz(q);                                                   \
+            tril[k] = __float_as_int(q.w);                                     \
+        }
+#else
+#define VPL_LOAD_NX() const f3* nxl = nx; const int* tril = tri_x;
+#endif
         if (VPL_VPL_CULL) {   // bounds of the block's front-face receivers and of their normals (uniform)
             const float inf = __int_as_float(0x7f800000);
             float lo[6] = {inf, inf, inf, inf, inf, inf}, hi[6] = {-inf, -inf, -inf, -inf, -inf, -inf};
@@ -188,22 +234,34 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
         TravStats st;
         unsigned long long n_traced = 0, n_vis = 0, n_pairs = 0;
         for (int ch = ch0; ch < ch1; ++ch) {
-        const int vbeg = ch * chunk, vend = min(M, vbeg + chunk);
-        if (kCount) n_pairs += (unsigned long long)__popc(act) * (unsigned long long)(vend - vbeg);
+        // The chunk's VPLs: groups of kGroup consecutive VPLs of the sorted copy, interleaved over the chunks
+        // (group q belongs to chunk q % n_chunks), so that every chunk samples the whole VPL set and the
+        // tasks of a block cost about the same — a contiguous range of the spatial order is either all
+        // culled or all near, and the longest tasks set the tail of a launch.  VPL_INTERLEAVE 0: contiguous.
+        const int n_groups = (M + kGroup - 1) / kGroup, gpc = chunk / kGroup;
+        const int q0 = VPL_INTERLEAVE ? ch : ch * gpc, q1 = VPL_INTERLEAVE ? n_groups : min(n_groups, (ch + 1) * gpc);
+        const int qs = VPL_INTERLEAVE ? n_chunks : 1;
 #pragma unroll
         for (int k = 0; k < kSeg; ++k) { s_acc[k][0][lane] = 0.0f; s_acc[k][1][lane] = 0.0f; s_acc[k][2][lane] = 0.0f; }
         if (__any_sync(0xFFFFFFFFu, act != 0)) {
-            for (int i0 = vbeg; i0 < vend; i0 += 256) {
+            for (int q = q0; q < q1; q += qs) {
+                const int i0 = q * kGroup, vend = M;
+                if (kCount) n_pairs += (unsigned long long)__popc(act) * (unsigned long long)(min(M, i0 + kGroup) - i0);
+#if !VPL_ACC_SMEM
                 float part[kSeg][3];
 #pragma unroll
                 for (int k = 0; k < kSeg; ++k) part[k][0] = part[k][1] = part[k][2] = 0.0f;
-                const int i1 = min(vend, i0 + 256);
+#endif
+                const int i1 = min(vend, i0 + kGroup);
                 for (int c0 = i0; c0 < i1; c0 += kCluster) {       // clusters of kCluster VPLs (i0 % 256 == 0)
                     const float4* cb = clusters ? clusters + 4 * (c0 / kCluster) : nullptr;
                     unsigned inc = act;                            // receivers that may trace the cluster
+                    {
+                        VPL_LOAD_NX();
 #pragma unroll
-                    for (int k = 0; k < kSeg; ++k)
-                        if (cb && ((inc >> k) & 1u) && !cluster_may_trace(cb, x[k], nx[k])) inc &= ~(1u << k);
+                        for (int k = 0; k < kSeg; ++k)
+                            if (cb && ((inc >> k) & 1u) && !cluster_may_trace(cb, x[k], nxl[k])) inc &= ~(1u << k);
+                    }
                     if (cb && !__any_sync(0xFFFFFFFFu, inc != 0)) continue;   // no receiver can trace any VPL of it
                     const int c1 = min(c0 + kCluster, i1);
                     int cand = -1, cand_end = cb ? c0 : INT_MAX;           // candidate list (lazy) and its VPL range end
@@ -214,11 +272,29 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                     unsigned need = 0xFFFFFFFFu >> (32 - (c1 - c0));
                     if (VPL_VPL_CULL && cb) need &= __ballot_sync(0xFFFFFFFFu, vpl_may_trace(vpls + min(c0 + lane, c1 - 1), s_rb));
                     while (need) {
+#if VPL_SCAN_LOOP
+                        // tight scan to the next VPL some receiver of the warp traces (cosine tests only)
+                        int i;
+                        float4 yv, nb;
+                        bool any;
+                        do {
+                            i = c0 + __ffs(need) - 1;
+                            need &= need - 1u;
+                            yv = __ldg((const float4*)(vpls + i));
+                            nb = __ldg((const float4*)(vpls + i) + 1);
+                            VPL_LOAD_NX();
+                            any = __any_sync(0xFFFFFFFFu, cosine_tests(xyz(yv), __float_as_int(yv.w), nb, x, nxl, tril, act) != 0);
+                        } while (!any && need);
+                        if (!any) break;
+                        VPL_LOAD_NX();
+#else
                         const int i = c0 + __ffs(need) - 1;
                         need &= need - 1u;
                         const float4 yv = __ldg((const float4*)(vpls + i)), nb = __ldg((const float4*)(vpls + i) + 1);
+                        VPL_LOAD_NX();
+#endif
                         float w[kSeg];
-                        const unsigned tv = shade<kCount>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), nb, x, nx, tri_x, act,
+                        const unsigned tv = shade<kCount>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), nb, x, nxl, tril, act,
                                                           eps, b2, cache, sstack, &st, w, cand, cand_end, c1, inc);
                         const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
                         if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
@@ -239,19 +315,28 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
 #pragma unroll
                             for (int k = 0; k < kSeg; ++k)
                                 if (vis & (1u << k)) {
+#if VPL_ACC_SMEM
+                                    s_acc[k][0][lane] = fmaf(phi.x, w[k], s_acc[k][0][lane]);
+                                    s_acc[k][1][lane] = fmaf(phi.y, w[k], s_acc[k][1][lane]);
+                                    s_acc[k][2][lane] = fmaf(phi.z, w[k], s_acc[k][2][lane]);
+#else
                                     part[k][0] = fmaf(phi.x, w[k], part[k][0]);
                                     part[k][1] = fmaf(phi.y, w[k], part[k][1]);
                                     part[k][2] = fmaf(phi.z, w[k], part[k][2]);
+#endif
                                 }
                         }
                     }
                 }
 #pragma unroll
                 for (int k = 0; k < kSeg; ++k) {
+#if !VPL_ACC_SMEM
                     s_acc[k][0][lane] += part[k][0]; s_acc[k][1][lane] += part[k][1]; s_acc[k][2][lane] += part[k][2];
+#endif
                 }
             }
         }
+#if VPL_TAIL_BLOCKS >= 0
         if (whole) {   // the same fold as the chunked path's: totals from 0.0f, chunk totals added in chunk order
 #pragma unroll
             for (int k = 0; k < kSeg; ++k) {
@@ -259,6 +344,7 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 s_tot[k][2][lane] += s_acc[k][2][lane];
             }
         }
+#endif
         }   // chunks of the task
         const float sc = (float)(1.0 / kPiR);
         if (whole) {
