@@ -716,19 +716,6 @@ __device__ __forceinline__ void cache_tests(const BvhView& bv, Segs& S, float ep
         test_tri<kCount, k, k + 1>(bv, S, S.pend & m, eps, cache[k].own1, cache, st);
 }
 
-// O13's cosine tests alone (the same operations as shade's first pass): bit k = receiver k traces the VPL
-__device__ __forceinline__ unsigned cosine_tests(f3 y, int yt, float4 nb, const f3* xr, const f3* nr, const int* tri_x,
-                                                 unsigned act) {
-    unsigned traced = 0;
-#pragma unroll
-    for (int k = 0; k < kSeg; ++k) {
-        const f3 d = y - xr[k];
-        const float cx = dot_fma(nr[k], d);
-        const float ci = -dot_fma(xyz(nb), d);
-        if (((act >> k) & 1u) && yt != tri_x[k] && cx > 0.0f && ci > 0.0f) traced |= 1u << k;
-    }
-    return traced;
-}
 #ifndef VPL_TWO_PASS
 #define VPL_TWO_PASS 1   // leave after the cosine tests when no receiver of the warp traces the VPL
 #endif

@@ -108,12 +108,6 @@ __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, floa
 #endif
 constexpr int kGroup = VPL_CHUNK_GROUP;
 static_assert(kGroup % kCluster == 0 && 256 % kGroup == 0, "interleave group");
-#ifndef VPL_NX_SMEM
-#define VPL_NX_SMEM 0
-#endif
-#ifndef VPL_SCAN_LOOP
-#define VPL_SCAN_LOOP 0   // inner loop over the VPLs no receiver of the warp traces (measured: C3 +3%, C4 +2%: off)
-#endif
 #ifndef VPL_ACC_SMEM
 #define VPL_ACC_SMEM 0   // 1: Eq. 1 sums accumulate in the shared-memory totals directly instead of 6 registers folded per
                          // group (measured: spills 268 -> 220 B but C4 +1.7%: off)
@@ -154,9 +148,6 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
     float (*s_tot)[3][32] = s_acc;         // whole-block tasks have a single chunk: its total is the block's
 #endif
     __shared__ float s_rb[12];             // receiver bounds of the task: lo(x, n), hi(x, n)  (VPL_VPL_CULL)
-#if VPL_NX_SMEM
-    __shared__ float4 s_nx[kSeg][32];      // receiver normal | triangle id
-#endif
     constexpr int kPart = 96 * kSeg;       // partial floats per (block, chunk): 32 lanes x kSeg receivers x 3
     const int lane = threadIdx.x;
     // Tasks: the first n_whole blocks of the call are whole-block tasks (one warp walks all the chunks of
@@ -194,24 +185,6 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             s_tot[k][0][lane] = 0.0f; s_tot[k][1][lane] = 0.0f; s_tot[k][2][lane] = 0.0f;
 #endif
         }
-#if VPL_NX_SMEM
-        // receiver normals and triangle ids live in shared memory (one LDS.128 per receiver where they are
-        // used) instead of 8 registers that the 64-register cap turns into per-VPL local-memory reloads
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < kSeg; ++k) s_nx[k][lane] = make_float4(nx[k].x, nx[k].y, nx[k].z, __int_as_float(tri_x[k]));
-        __syncwarp();
-#define VPL_LOAD_NX()                                                          \
-        f3 nxl[kSeg];                                                          \
-        int tril[kSeg];                                                        \
-        _Pragma("unroll") for (int k = 0; k < kSeg; ++k) {                     \
-            const float4 q = s_nx[k][lane];                                    \
-            nxl[k] = xyz(q);                                                   \
-            tril[k] = __float_as_int(q.w);                                     \
-        }
-#else
-#define VPL_LOAD_NX() const f3* nxl = nx; const int* tril = tri_x;
-#endif
         if (VPL_VPL_CULL) {   // bounds of the block's front-face receivers and of their normals (uniform)
             const float inf = __int_as_float(0x7f800000);
             float lo[6] = {inf, inf, inf, inf, inf, inf}, hi[6] = {-inf, -inf, -inf, -inf, -inf, -inf};
@@ -256,12 +229,9 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                 for (int c0 = i0; c0 < i1; c0 += kCluster) {       // clusters of kCluster VPLs (i0 % 256 == 0)
                     const float4* cb = clusters ? clusters + 4 * (c0 / kCluster) : nullptr;
                     unsigned inc = act;                            // receivers that may trace the cluster
-                    {
-                        VPL_LOAD_NX();
 #pragma unroll
-                        for (int k = 0; k < kSeg; ++k)
-                            if (cb && ((inc >> k) & 1u) && !cluster_may_trace(cb, x[k], nxl[k])) inc &= ~(1u << k);
-                    }
+                    for (int k = 0; k < kSeg; ++k)
+                        if (cb && ((inc >> k) & 1u) && !cluster_may_trace(cb, x[k], nx[k])) inc &= ~(1u << k);
                     if (cb && !__any_sync(0xFFFFFFFFu, inc != 0)) continue;   // no receiver can trace any VPL of it
                     const int c1 = min(c0 + kCluster, i1);
                     int cand = -1, cand_end = cb ? c0 : INT_MAX;           // candidate list (lazy) and its VPL range end
@@ -272,29 +242,11 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                     unsigned need = 0xFFFFFFFFu >> (32 - (c1 - c0));
                     if (VPL_VPL_CULL && cb) need &= __ballot_sync(0xFFFFFFFFu, vpl_may_trace(vpls + min(c0 + lane, c1 - 1), s_rb));
                     while (need) {
-#if VPL_SCAN_LOOP
-                        // tight scan to the next VPL some receiver of the warp traces (cosine tests only)
-                        int i;
-                        float4 yv, nb;
-                        bool any;
-                        do {
-                            i = c0 + __ffs(need) - 1;
-                            need &= need - 1u;
-                            yv = __ldg((const float4*)(vpls + i));
-                            nb = __ldg((const float4*)(vpls + i) + 1);
-                            VPL_LOAD_NX();
-                            any = __any_sync(0xFFFFFFFFu, cosine_tests(xyz(yv), __float_as_int(yv.w), nb, x, nxl, tril, act) != 0);
-                        } while (!any && need);
-                        if (!any) break;
-                        VPL_LOAD_NX();
-#else
                         const int i = c0 + __ffs(need) - 1;
                         need &= need - 1u;
                         const float4 yv = __ldg((const float4*)(vpls + i)), nb = __ldg((const float4*)(vpls + i) + 1);
-                        VPL_LOAD_NX();
-#endif
                         float w[kSeg];
-                        const unsigned tv = shade<kCount>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), nb, x, nxl, tril, act,
+                        const unsigned tv = shade<kCount>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), nb, x, nx, tri_x, act,
                                                           eps, b2, cache, sstack, &st, w, cand, cand_end, c1, inc);
                         const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
                         if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }

@@ -114,9 +114,9 @@ def test_frozen_o0_parity(cfg):
 
 @pytest.mark.parametrize("cfg", [3, 4])
 def test_cull_and_lists_exact(cfg):
-    """Whole frame: the VPL-cluster cull and the per-cluster candidate lists change no traced or
-    visible pair (counters equal to a run with plain per-VPL traversal) and the image is bitwise
-    the same."""
+    """Whole frame: the VPL-cluster cull, the per-VPL cull, the per-run candidate lists and the
+    plane-side cull of list entries change no traced or visible pair (counters equal to a run with
+    plain per-VPL traversal and an exact MT for every box hit) and the image is bitwise the same."""
     s, r, _, _, _, _, _ = _frame(cfg)
     rgb_a, ca, _, _ = V.gather_dump(r.scene, r.bvh, r.gbuf, r.vpls, r.tiles, s.width, s.height)
     rgb_b, cb, _, _ = V.gather_dump(r.scene, r.bvh, r.gbuf, r.vpls, r.tiles, s.width, s.height, no_cull=True)
@@ -125,6 +125,7 @@ def test_cull_and_lists_exact(cfg):
     for k in ("pairs", "traced", "visible"):
         assert a[k] == b[k], (k, a[k], b[k])
     assert a["cand_lists"] > 0 and b["cand_lists"] == 0
+    assert a["plane_culled"] > 0 and b["plane_culled"] == 0      # the plane-side cull ran (and only in the default run)
     assert torch.equal(rgb_a, rgb_b)
     assert torch.equal(rgb_a, r.rgb)
 
