@@ -179,7 +179,9 @@ VPL_API int32_t vpl_scene_consts(const void* d_scene, double* diag, float* eps, 
  * of the centroids, SAH leaf collapse, then a 16-wide (beam traversal) and a
  * 4-wide (per-ray traversal) collapse of the same tree; boxes padded by
  * 2^-16 * max|coord| so every box test is conservative w.r.t. the exact
- * Moller-Trumbore tests of O9.  Same scene in, same bytes out.
+ * Moller-Trumbore tests of O9; per triangle also its plane (unit normal and
+ * offset, rounded once from float64) for the gather's plane-side cull.
+ * Same scene in, same bytes out.
  * d_bvh: vpl_bvh_bytes(...).bvh bytes; d_work: .work bytes (scratch). */
 VPL_API int32_t vpl_bvh_bytes(int64_t n_tris, size_t* bvh_bytes, size_t* work_bytes);
 VPL_API int32_t vpl_build_bvh(const void* d_scene, void* d_bvh, size_t bvh_bytes, void* d_work, size_t work_bytes,
@@ -222,14 +224,17 @@ VPL_API int32_t vpl_render_gbuffer(const void* d_scene, const void* d_bvh, const
  * d_work: vpl_gather_bytes(n_vpls, W, H) bytes (tile queue, a Morton-ordered
  * copy of the VPLs — Eq. 1 is a sum over the set, the gather visits it in
  * spatial order; the caller's array is not modified — VPL cluster bounds and,
- * when M > 256, per-chunk partial sums: the work items are (8x4 pixel block,
- * VPL chunk) pairs, chunk = max(256, ceil(M/128) rounded up to 256), folded in
- * chunk order by the warp that completes a block's last chunk, so the image
- * depends on M only, never on the tile split; the partial sums live in a
- * ring of 4096 block slots reused in block order).  Visibility of each traced
- * pair is the exact O9 any-hit: the 16-wide BVH is culled with conservative
- * beams (padded boxes) and, per run of 16 consecutive sorted VPLs, a list of
- * candidate triangles gathered once with the run's beam. */
+ * when M > 256, per-chunk partial sums: the work items are (8x8 pixel block,
+ * VPL chunk) pairs, chunk = max(256, ceil(M/128) rounded up to 256) VPLs —
+ * groups of 128 consecutive sorted VPLs dealt round-robin to the chunks —
+ * folded in chunk order by the warp that completes a block's last chunk, so
+ * the image depends on M only, never on the tile split; the partial sums live
+ * in a ring of 4096 block slots reused in block order).  Visibility of each
+ * traced pair is the exact O9 any-hit: the 16-wide BVH is culled with
+ * conservative beams (padded boxes); per run of 16 consecutive sorted VPLs a
+ * list of candidate triangles is gathered once with the run's beam; a list
+ * entry whose plane no pending segment can cross inside (eps, L - eps) is
+ * skipped before its MT tests. */
 VPL_API int32_t vpl_gather_bytes(int32_t n_vpls, int32_t width, int32_t height, size_t* work_bytes);
 VPL_API int32_t vpl_gather_indirect(const void* d_scene, const void* d_bvh, const vpl_gpoint* d_gbuf,
                             const vpl_record* d_vpls, int32_t n_vpls, const int32_t* d_tiles, int32_t n_tiles,

@@ -716,33 +716,42 @@ __device__ __forceinline__ void cache_tests(const BvhView& bv, Segs& S, float ep
         test_tri<kCount, k, k + 1>(bv, S, S.pend & m, eps, cache[k].own1, cache, st);
 }
 
-#ifndef VPL_TWO_PASS
-#define VPL_TWO_PASS 1   // leave after the cosine tests when no receiver of the warp traces the VPL
-#endif
 // One VPL (position y, triangle yt; uniform) for one lane's receivers: Eq. 1 terms (O13, exact fp32
-// order), segment setup (O9), occluder caches, resolution.  act: bit k = receiver k is a front-face
-// hit; nb: the VPL's normal record (loaded by the caller, one VPL ahead).  Returns traced | vis << 16
-// (bit k per receiver) and w[k] = cx*ci / (r2 * max(r2, b2)).
-template <bool kCount>
-__device__ __forceinline__ unsigned shade(const BvhView& bv, const vpl_record* __restrict__ vpls, int i, f3 y, int yt,
-                                          float4 nb, const f3* xr, const f3* nr, const int* tri_x, unsigned act, float eps,
-                                          float b2, OccluderCache* cache, int* __restrict__ sstack, TravStats* st,
-                                          float* w, int& cand, int& cand_end, int cend, unsigned part) {
-    // pass 1: the cosine tests only (most VPLs are traced by no receiver of the warp: nothing else is
-    // computed or stored for them)
-    unsigned traced = 0;
-#pragma unroll
-    for (int k = 0; k < kSeg; ++k) {
-        const f3 d = y - xr[k];
-        const float cx = dot_fma(nr[k], d);          // R26: the cosine terms as fused dots
-        const float ci = -dot_fma(xyz(nb), d);
-        w[k] = cx * ci;
-        if (((act >> k) & 1u) && yt != tri_x[k] && cx > 0.0f && ci > 0.0f) traced |= 1u << k;
-    }
-#if VPL_TWO_PASS
-    if (!__any_sync(0xFFFFFFFFu, traced != 0)) return 0;
+// order), segment setup (O9), occluder caches, resolution — in two functions.  `shade` (inlined in the
+// kernel's VPL loop) evaluates the two cosine tests; only if some receiver of the warp traces the VPL it
+// calls `shade_heavy`: segment setup, cache tests, lists, filter, traversals, MT.  The state only the
+// heavy part touches (occluder caches, candidate-list cursor, the weights) is grouped in a HeavyState.
+// (VPL_HEAVY_NOINLINE = 1 compiles shade_heavy out of line, with a register allocation of its own and
+// the HeavyState in local memory: measured, slower — see the knob.)
+#ifndef VPL_HEAVY_NOINLINE
+#define VPL_HEAVY_NOINLINE 0   // measured at 1: ptxas then keeps every value that lives across the call in local memory
+                               // (17 reloads per VPL in the light loop instead of 11) and the call itself costs: C4 652 ->
+                               // 870 ms, C3 220 -> 286 ms.  0: inlined (the HeavyState is then scalarised into registers).
 #endif
-    // pass 2: Eq. 1 weight and segment setup of the traced receivers
+struct HeavyState {
+    OccluderCache cache[kSeg];
+    float w[kSeg];        // in: cx * ci of the traced receivers; out: w = cx*ci / (r2 * max(r2, b2))
+    int cand, cand_end;   // the run's candidate list (length or -1) and the VPL index its run ends at
+    float eps, b2;
+};
+struct RecvPos { f3 x[kSeg]; };
+
+template <bool kCount>
+#if VPL_HEAVY_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+unsigned shade_heavy(const BvhView& bv, const vpl_record* __restrict__ vpls, int i, f3 y, RecvPos X, unsigned traced,
+                     int cend, unsigned part, HeavyState* __restrict__ hs, int* __restrict__ sstack, TravStats* st) {
+    const float eps = hs->eps, b2 = hs->b2;
+    const f3* xr = X.x;
+    OccluderCache cache[kSeg];
+    float w[kSeg];
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) { cache[k] = hs->cache[k]; w[k] = hs->w[k]; }
+    int cand = hs->cand, cand_end = hs->cand_end;
+    // Eq. 1 weight and segment setup of the traced receivers
     Segs S;
     S.pend = 0; S.occ = 0;
 #pragma unroll
@@ -769,9 +778,6 @@ __device__ __forceinline__ unsigned shade(const BvhView& bv, const vpl_record* _
             if (S.tmax[k] > eps) S.pend |= 1u << k;
         }
     }
-#if !VPL_TWO_PASS
-    if (!__any_sync(0xFFFFFFFFu, traced != 0)) return 0;
-#endif
     // occluder caches: exact MT of each receiver's segment against its recent occluders; a receiver
     // whose last traced segment was visible skips its cache (visibility is coherent along the
     // spatially ordered VPLs)
@@ -788,7 +794,36 @@ __device__ __forceinline__ unsigned shade(const BvhView& bv, const vpl_record* _
     for (int k = 0; k < kSeg; ++k)
         if (traced & (1u << k)) cache[k].vis_streak = (vis >> k) & 1u;
 #endif
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) { hs->cache[k] = cache[k]; hs->w[k] = w[k]; }
+    hs->cand = cand; hs->cand_end = cand_end;
     return traced | vis << 16;
+}
+
+// act: bit k = receiver k is a front-face hit; nb: the VPL's normal record.  Returns traced | vis << 16
+// (bit k per receiver); the weights of the visible receivers are in hs->w.
+template <bool kCount>
+__device__ __forceinline__ unsigned shade(const BvhView& bv, const vpl_record* __restrict__ vpls, int i, f3 y, int yt,
+                                          float4 nb, const f3* xr, const f3* nr, const int* tri_x, unsigned act,
+                                          HeavyState* hs, int* __restrict__ sstack, TravStats* st, int cend,
+                                          unsigned part) {
+    // the cosine tests only (most VPLs are traced by no receiver of the warp: nothing else is computed
+    // or stored for them)
+    unsigned traced = 0;
+    float wp[kSeg];
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) {
+        const f3 d = y - xr[k];
+        const float cx = dot_fma(nr[k], d);          // R26: the cosine terms as fused dots
+        const float ci = -dot_fma(xyz(nb), d);
+        wp[k] = cx * ci;
+        if (((act >> k) & 1u) && yt != tri_x[k] && cx > 0.0f && ci > 0.0f) traced |= 1u << k;
+    }
+    if (!__any_sync(0xFFFFFFFFu, traced != 0)) return 0;
+    RecvPos X;
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) { X.x[k] = xr[k]; hs->w[k] = wp[k]; }
+    return shade_heavy<kCount>(bv, vpls, i, y, X, traced, cend, part, hs, sstack, st);
 }
 
 }  // namespace vplgi

@@ -203,7 +203,10 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
             }
             __syncwarp();
         }
-        OccluderCache cache[kSeg];
+        HeavyState hs;   // occluder caches, list cursor, weights: touched by shade_heavy only (local memory)
+#pragma unroll
+        for (int k = 0; k < kSeg; ++k) hs.cache[k] = OccluderCache();
+        hs.eps = eps; hs.b2 = b2;
         TravStats st;
         unsigned long long n_traced = 0, n_vis = 0, n_pairs = 0;
         for (int ch = ch0; ch < ch1; ++ch) {
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                         if (cb && ((inc >> k) & 1u) && !cluster_may_trace(cb, x[k], nx[k])) inc &= ~(1u << k);
                     if (cb && !__any_sync(0xFFFFFFFFu, inc != 0)) continue;   // no receiver can trace any VPL of it
                     const int c1 = min(c0 + kCluster, i1);
-                    int cand = -1, cand_end = cb ? c0 : INT_MAX;           // candidate list (lazy) and its VPL range end
+                    hs.cand = -1; hs.cand_end = cb ? c0 : INT_MAX;         // candidate list (lazy) and its VPL range end
                     // per-VPL cull, transposed: lane l tests VPL c0 + l against the box of the block's
                     // receivers and the box of their normals (s_rb) — can cx > 0 and ci > 0 hold for any
                     // of them?  Same conservative margin as the cluster cull; the VPL loop then visits
@@ -245,9 +248,9 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                         const int i = c0 + __ffs(need) - 1;
                         need &= need - 1u;
                         const float4 yv = __ldg((const float4*)(vpls + i)), nb = __ldg((const float4*)(vpls + i) + 1);
-                        float w[kSeg];
                         const unsigned tv = shade<kCount>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), nb, x, nx, tri_x, act,
-                                                          eps, b2, cache, sstack, &st, w, cand, cand_end, c1, inc);
+                                                          &hs, sstack, &st, c1, inc);
+                        const float* w = hs.w;
                         const unsigned tr = tv & 0xFFFFu, vis = tv >> 16;
                         if (kCount) { n_traced += __popc(tr); n_vis += __popc(vis); }
                         if (kDump) {
@@ -398,7 +401,9 @@ __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict
     __shared__ int s_stack[2][kWarpStack];
     int* sstack = s_stack[threadIdx.x >> 5];
     int64_t words = (M + 31) / 32;
-    OccluderCache cache[kSeg];
+    HeavyState hs;
+#pragma unroll
+    for (int q = 0; q < kSeg; ++q) hs.cache[q] = OccluderCache();
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     if ((k - lane) >= n_px) return;                      // whole warp out of range
@@ -410,15 +415,15 @@ __global__ void k_visdump(SceneView sv, BvhView bv, const vpl_gpoint* __restrict
     if (kSeg > 1) { x[kSeg - 1] = x[0]; nx[kSeg - 1] = nx[0]; tri_x[kSeg - 1] = -1; }
     const unsigned act = (inb && gp->tri >= 0 && gp->front) ? 1u : 0u;
     const float eps = sv.hdr->eps, b2 = sv.hdr->b2;
+    hs.eps = eps; hs.b2 = b2;
     for (int64_t wd = 0; wd < words; ++wd) {
         uint32_t tb = 0, vb = 0;
         const int i0 = (int)(wd * 32), i1 = min(M, i0 + 32);
         for (int i = i0; i < i1; ++i) {
             const float4 yv = __ldg((const float4*)(vpls + i)), nb = __ldg((const float4*)(vpls + i) + 1);
-            float w[kSeg];
-            int cand = -1, cand_end = INT_MAX;
-            const unsigned tv = shade<false>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), nb, x, nx, tri_x, act, eps, b2,
-                                             cache, sstack, nullptr, w, cand, cand_end, i1, act);
+            hs.cand = -1; hs.cand_end = INT_MAX;
+            const unsigned tv = shade<false>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), nb, x, nx, tri_x, act, &hs,
+                                             sstack, nullptr, i1, act);
             tb |= (tv & 1u) << (i - i0);
             vb |= ((tv >> 16) & 1u) << (i - i0);
         }
