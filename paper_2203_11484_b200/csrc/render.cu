@@ -108,6 +108,10 @@ __global__ void k_vpl_clusters(const vpl_record* __restrict__ v, int32_t M, floa
 #endif
 constexpr int kGroup = VPL_CHUNK_GROUP;
 static_assert(kGroup % kCluster == 0 && 256 % kGroup == 0, "interleave group");
+#ifndef VPL_STAGE
+#define VPL_STAGE 0   // 1: each cluster's VPL records staged in shared memory by a 1-D bulk async copy (cp.async.bulk +
+                      // mbarrier; single buffer, the copy overlaps the per-VPL cull) instead of warp-uniform L1 loads
+#endif
 #ifndef VPL_ACC_SMEM
 #define VPL_ACC_SMEM 0   // 1: Eq. 1 sums accumulate in the shared-memory totals directly instead of 6 registers folded per
                          // group (measured: spills 268 -> 220 B but C4 +1.7%: off)
@@ -148,6 +152,18 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
     float (*s_tot)[3][32] = s_acc;         // whole-block tasks have a single chunk: its total is the block's
 #endif
     __shared__ float s_rb[12];             // receiver bounds of the task: lo(x, n), hi(x, n)  (VPL_VPL_CULL)
+#if VPL_STAGE
+    __shared__ __align__(128) float4 s_vpl[3 * kCluster];   // the current cluster's records, staged by a bulk async copy
+    __shared__ __align__(8) unsigned long long s_bar;       // its mbarrier (one arrival + the copy's bytes per phase)
+    const unsigned s_vpl_addr = (unsigned)__cvta_generic_to_shared(s_vpl);
+    const unsigned s_bar_addr = (unsigned)__cvta_generic_to_shared(&s_bar);
+    unsigned stage_phase = 0;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_bar_addr) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+#endif
     constexpr int kPart = 96 * kSeg;       // partial floats per (block, chunk): 32 lanes x kSeg receivers x 3
     const int lane = threadIdx.x;
     // Tasks: the first n_whole blocks of the call are whole-block tasks (one warp walks all the chunks of
@@ -243,11 +259,38 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                     // of them?  Same conservative margin as the cluster cull; the VPL loop then visits
                     // only the VPLs some receiver may trace.
                     unsigned need = 0xFFFFFFFFu >> (32 - (c1 - c0));
+#if VPL_STAGE
+                    // the cluster's records (48 B each) by one 1-D bulk async copy (TMA) into shared memory;
+                    // the copy overlaps the per-VPL cull below, its completion is awaited on the mbarrier
+                    __syncwarp();   // the previous cluster's readers are done
+                    if (lane == 0) {
+                        const unsigned bytes = (unsigned)(c1 - c0) * 48u;
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_bar_addr), "r"(bytes) : "memory");
+                        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                     ::"r"(s_vpl_addr), "l"(vpls + c0), "r"(bytes), "r"(s_bar_addr) : "memory");
+                    }
+#endif
                     if (VPL_VPL_CULL && cb) need &= __ballot_sync(0xFFFFFFFFu, vpl_may_trace(vpls + min(c0 + lane, c1 - 1), s_rb));
+#if VPL_STAGE
+                    {
+                        unsigned ok = 0;
+                        for (int spin = 0; !ok; ++spin) {
+                            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                                         : "=r"(ok) : "r"(s_bar_addr), "r"(stage_phase) : "memory");
+                            if (spin > (1 << 22)) __trap();   // never hang the GPU on a lost copy
+                        }
+                        stage_phase ^= 1u;
+                    }
+#endif
                     while (need) {
                         const int i = c0 + __ffs(need) - 1;
                         need &= need - 1u;
+#if VPL_STAGE
+                        const float4 yv = s_vpl[3 * (i - c0)], nb = s_vpl[3 * (i - c0) + 1];
+#else
                         const float4 yv = __ldg((const float4*)(vpls + i)), nb = __ldg((const float4*)(vpls + i) + 1);
+#endif
                         const unsigned tv = shade<kCount>(bv, vpls, i, xyz(yv), __float_as_int(yv.w), nb, x, nx, tri_x, act,
                                                           &hs, sstack, &st, c1, inc);
                         const float* w = hs.w;
@@ -266,7 +309,11 @@ __global__ void __launch_bounds__(32, VPL_GATHER_CTAS) k_gather(SceneView sv, Bv
                             }
                         }
                         if (vis) {
+#if VPL_STAGE
+                            const float4 phi = s_vpl[3 * (i - c0) + 2];
+#else
                             const float4 phi = __ldg((const float4*)(vpls + i) + 2);
+#endif
 #pragma unroll
                             for (int k = 0; k < kSeg; ++k)
                                 if (vis & (1u << k)) {
