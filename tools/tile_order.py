@@ -45,6 +45,9 @@ for cfg in a.configs:
         "super4x4": t[np.lexsort((x % 4, y % 4, x // 4, y // 4))],
         "super8x8": t[np.lexsort((x % 8, y % 8, x // 8, y // 8))],
         "column-major": t[np.lexsort((y, x))],
+        "random": np.random.default_rng(7).permutation(t).astype(np.int32),
+        "random-eighth": np.sort(np.random.default_rng(7).permutation(t)[: len(t) // 8]).astype(np.int32),
+        "super4x4-eighth": t[((x // 4 + (y // 4) * ((tx + 3) // 4)) % 8) == 0],
     }
     out = {"config": cfg}
     for name, order in orders.items():
@@ -57,5 +60,6 @@ for cfg in a.configs:
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
-        out[name] = {"ms": min(ts), "bitwise_equal": bool(torch.equal(r.rgb, ref))}
+        out[name] = {"ms": min(ts), "tiles": int(len(order)),
+                     "bitwise_equal": bool(torch.equal(r.rgb, ref)) if len(order) == len(t) else None}
     print(json.dumps(out), flush=True)
