@@ -235,8 +235,9 @@ def run_ours(args):
             r.vpls = vbuf[: n_out * V.VPL_RECORD_BYTES].view(-1, V.VPL_RECORD_BYTES)
         V.render_gbuffer(r.scene, r.bvh, r.tiles, W, H, tw, th, r.gbuf, stream)
         ev["gather"][0].record(stream)
+        r._gawork = V.gather_work(r.vpls, W, H, dev, getattr(r, "_gawork", None))   # persistent scratch
         r.rgb, r.ctr = V.gather_indirect(r.scene, r.bvh, r.gbuf, r.vpls, r.tiles, W, H, tw, th, r.rgb, counters,
-                                         stream=stream)
+                                         work=r._gawork, stream=stream)
         ev["gather"][1].record(stream)
         assembler(r.rgb, rank, dst=0)
         return r.rgb

@@ -274,6 +274,17 @@ def render_gbuffer(scene, bvh, tiles, W, H, tw=16, th=16, gbuf=None, stream=None
     return gbuf
 
 
+def gather_work(vpls, W, H, device, work=None):
+    """The gather's scratch buffer (vpl_gather_bytes) for the VPL tensor `vpls`: `work` if it is large enough,
+    else a new tensor."""
+    nv = vpls.shape[0] if vpls.dim() == 2 else vpls.numel() // VPL_RECORD_BYTES
+    wb = C.c_size_t()
+    _check(load_library().vpl_gather_bytes(int(nv), W, H, C.byref(wb)), "vpl_gather_bytes")
+    if work is None or work.numel() < wb.value:
+        work = torch.empty(wb.value, dtype=torch.uint8, device=device)
+    return work
+
+
 def gather_indirect(scene, bvh, gbuf, vpls, tiles, W, H, tw=16, th=16, rgb=None, counters=False, work=None,
                     stream=None):
     dev = scene.device
@@ -495,6 +506,8 @@ class Renderer:
             self.scene, self.bvh, self.labels, self.n, self.s.M, self.s.K_near, self.s.max_depth, self.s.rr,
             self.s.seed, max_out=self.max_out, vpls=self._vbuf, work=self._gwork, stream=stream)
         render_gbuffer(self.scene, self.bvh, self.tiles, self.W, self.H, self.tw, self.th, self.gbuf, stream)
+        # one persistent gather scratch buffer per renderer (0.4 GB at C4), not one per call
+        self._gawork = gather_work(self.vpls, self.W, self.H, self.device, getattr(self, "_gawork", None))
         self.rgb, self.ctr = gather_indirect(self.scene, self.bvh, self.gbuf, self.vpls, self.tiles, self.W, self.H,
-                                             self.tw, self.th, self.rgb, counters, stream=stream)
+                                             self.tw, self.th, self.rgb, counters, work=self._gawork, stream=stream)
         return self.rgb
